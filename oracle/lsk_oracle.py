@@ -1,0 +1,295 @@
+"""ORACLE — plain, slow, fp64 CPU reference of the factored-Sinkhorn hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and bench.py's
+``cpu_baseline`` / ``--impl reference`` leg may import this module.  The product package
+(``paper_2006_07057_b200``) never imports it and shares no code, header, table or constant
+generator with it; the only shared module is ``synth`` (seeded inputs, no method arithmetic).
+
+Every function follows the paper's order and notation (PAPER.md = arXiv 2006.07057 LaTeX in
+/root/reference; line numbers cite the full-paper fragment).  Layout
+follows the paper: feature matrices are r x n, xi = [phi_theta(x_1), ..., phi_theta(x_n)]
+(PAPER.md:278), so K_theta = xi^T zeta.  Arithmetic is fp64 throughout; fp32
+inputs are promoted.  Library primitives used as single steps: numpy matmul / exp / log,
+numpy's Philox-free integer ops.  No blocking, fusion or reordering.
+
+Readings of silent/garbled passages are the C-numbered items of DESIGN.md §Readings.
+
+Pins (tests/test_oracle_*.py) — every function below is pinned to something outside itself:
+  lambert_w0            scipy.special.lambertw, W(1)=Omega constant, residual  (P1)
+  gaussian_params       q = e^{W0(z)}/2 identity, q W0 2 eps d = R^2            (P2)
+  gaussian_phi          phi(0,0)=(2q)^{d/4}; Gauss-Hermite kernel identity;     (P3,P4,P6)
+                        ratio bound 2(2q)^{d/2}
+  philox4x32_10         Random123 known-answer vectors (tests/golden/philox_kat.txt)
+  standard_normals      moment test + Box-Muller closed form on known words
+  feature_matrix        == gaussian_phi per entry; Monte-Carlo rate slope -1/2   (P5,P7)
+  sinkhorn_*            dense == factored (P8), n=m=1 (P9), 2x2 closed form (P10),
+                        rank-1 closed form (P11), marginals (P12), convergence (P13),
+                        primal == dual (P14), gauge invariance (P15), dual range (P17)
+  dual_estimate         P9/P10/P11/P14
+  exact gaussian ROT    paper RE behaviour on the Fig. 1 setup (P16, qualitative: the
+                        paper prints no numbers — "parity unpinned" for the RE values
+                        themselves; only the sign/monotonic trends are asserted)
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, Optional
+
+import numpy as np
+
+LOG2E = 1.0 / math.log(2.0)
+
+
+# ---------------------------------------------------------------------------------------
+# a1. Feature parameters: Lambert W_0, q, sigma (Lemma decomp-RBF)
+# ---------------------------------------------------------------------------------------
+def lambert_w0(z: float, tol: float = 1e-15, max_iter: int = 100) -> float:
+    """Principal branch W_0(z): the w >= -1 with w e^w = z ("W_0 is the Lambert
+    function"; positive real branch).  Halley iteration from log(1+z) for
+    z >= 0 (the only domain the feature map uses; z = R^2/(eps d) > 0)."""
+    if z < -1.0 / math.e:
+        raise ValueError("lambert_w0: z < -1/e")
+    if z == 0.0:
+        return 0.0
+    w = math.log1p(z) if z > 0 else -0.5
+    for _ in range(max_iter):
+        ew = math.exp(w)
+        f = w * ew - z
+        wp1 = w + 1.0
+        denom = ew * wp1 - (w + 2.0) * f / (2.0 * wp1)
+        step = f / denom
+        w -= step
+        if abs(step) <= tol * (1.0 + abs(w)):
+            break
+    return w
+
+
+def max_norm(X: np.ndarray, Y: np.ndarray) -> float:
+    """R = max over both clouds of the Euclidean norm (reading C3), fp64 from fp32 inputs."""
+    X = np.asarray(X, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    return float(max(np.sqrt((X * X).sum(axis=1)).max(), np.sqrt((Y * Y).sum(axis=1)).max()))
+
+
+def gaussian_params(eps: float, d: int, r: int, R: float) -> dict:
+    """q = R^2 / (2 eps d W_0(R^2/(eps d)));  sigma^2 = q eps / 4
+    (rho_q = N(0, q/(4 eps^-1) Id));
+    log_scale = (d/4) ln(2q) - (1/2) ln r  collects the (2q)^{d/4} factor of phi
+     and the 1/sqrt(r) of phi_theta."""
+    z = R * R / (eps * d)
+    W = lambert_w0(z)
+    q = z / (2.0 * W)
+    sigma = math.sqrt(q * eps / 4.0)
+    log_scale = 0.25 * d * math.log(2.0 * q) - 0.5 * math.log(r)
+    return dict(z=z, W=W, q=q, sigma=sigma, log_scale=log_scale, R=R, eps=eps, d=d, r=r)
+
+
+# ---------------------------------------------------------------------------------------
+# a2. Anchors u_1..u_r ~ rho = N(0, sigma^2 Id), i.i.d.
+#     Reading C5: counter-based Philox4x32-10 + fp64 Box-Muller, rounded to fp32.
+# ---------------------------------------------------------------------------------------
+_PHILOX_M0 = np.uint64(0xD2511F53)
+_PHILOX_M1 = np.uint64(0xCD9E8D57)
+_PHILOX_W0 = 0x9E3779B9
+_PHILOX_W1 = 0xBB67AE85
+_MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr: np.ndarray, key) -> np.ndarray:
+    """Philox4x32 with 10 rounds (Salmon, Moraes, Dror, Shaw, SC'11).  ``ctr`` is (N,4)
+    uint32, ``key`` is (k0,k1).  One round: (hi0,lo0)=M0*c0, (hi1,lo1)=M1*c2,
+    c <- (hi1^c1^k0, lo1, hi0^c3^k1, lo0); between rounds k <- k + (W0,W1) mod 2^32."""
+    c = np.asarray(ctr, dtype=np.uint64).reshape(-1, 4).copy()
+    k0, k1 = int(key[0]) & 0xFFFFFFFF, int(key[1]) & 0xFFFFFFFF
+    for rnd in range(10):
+        if rnd > 0:
+            k0 = (k0 + _PHILOX_W0) & 0xFFFFFFFF
+            k1 = (k1 + _PHILOX_W1) & 0xFFFFFFFF
+        p0 = _PHILOX_M0 * c[:, 0]
+        p1 = _PHILOX_M1 * c[:, 2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & _MASK32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & _MASK32
+        n0 = hi1 ^ c[:, 1] ^ np.uint64(k0)
+        n2 = hi0 ^ c[:, 3] ^ np.uint64(k1)
+        c = np.stack([n0, lo1, n2, lo0], axis=1)
+    return c.astype(np.uint32)
+
+
+def philox_words(r: int, d: int, seed: int) -> np.ndarray:
+    """Raw words for anchors: counter (k, p, 0, 0) for anchor k and coordinate block
+    p = 0..ceil(d/4)-1, key = (seed mod 2^32, seed >> 32).  Returns (r, P, 4) uint32."""
+    P = (d + 3) // 4
+    kk, pp = np.meshgrid(np.arange(r, dtype=np.uint64), np.arange(P, dtype=np.uint64),
+                         indexing="ij")
+    ctr = np.stack([kk.ravel(), pp.ravel(), np.zeros(r * P, np.uint64),
+                    np.zeros(r * P, np.uint64)], axis=1)
+    key = (seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    return philox4x32_10(ctr, key).reshape(r, P, 4)
+
+
+def standard_normals(r: int, d: int, seed: int) -> np.ndarray:
+    """Box-Muller in fp64 on each word pair: u1 = (w0+1) 2^-32 in (0,1], u2 = w1 2^-32,
+    z = sqrt(-2 ln u1) (cos 2 pi u2, sin 2 pi u2); the same for (w2, w3).  Coordinates
+    4p..4p+3 of anchor k come from block p.  Returns (r, d) fp64."""
+    w = philox_words(r, d, seed).astype(np.float64)
+    u1a = (w[..., 0] + 1.0) * 2.0 ** -32
+    u2a = w[..., 1] * 2.0 ** -32
+    u1b = (w[..., 2] + 1.0) * 2.0 ** -32
+    u2b = w[..., 3] * 2.0 ** -32
+    ra = np.sqrt(-2.0 * np.log(u1a))
+    rb = np.sqrt(-2.0 * np.log(u1b))
+    z = np.stack([ra * np.cos(2.0 * np.pi * u2a), ra * np.sin(2.0 * np.pi * u2a),
+                  rb * np.cos(2.0 * np.pi * u2b), rb * np.sin(2.0 * np.pi * u2b)], axis=-1)
+    return z.reshape(r, -1)[:, :d]
+
+
+def draw_anchors(r: int, d: int, sigma: float, seed: int) -> np.ndarray:
+    """theta = (u_1..u_r), u_k ~ N(0, sigma^2 Id) i.i.d.; values are
+    rounded to fp32 (the stored precision) and returned promoted to fp64, shape (r, d)."""
+    return (sigma * standard_normals(r, d, seed)).astype(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------------------
+# a3. Gaussian positive feature map (Lemma decomp-RBF, appendix form PAPER.md:915, 934;
+#     reading C1: the main-text exponent at PAPER.md:389 is garbled)
+# ---------------------------------------------------------------------------------------
+def gaussian_phi(x: np.ndarray, u: np.ndarray, eps: float, q: float) -> np.ndarray:
+    """phi(x,u) = (2q)^{d/4} exp(-2 eps^-1 |x-u|^2) exp(eps^-1 |u|^2 / q).
+    Broadcasts over leading axes of x and u (last axis = coordinates)."""
+    x = np.asarray(x, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    d = x.shape[-1]
+    sq = ((x - u) ** 2).sum(axis=-1)
+    uu = (u * u).sum(axis=-1)
+    return (2.0 * q) ** (d / 4.0) * np.exp(-2.0 / eps * sq) * np.exp(uu / (eps * q))
+
+
+def feature_matrix(X: np.ndarray, U: np.ndarray, eps: float, q: float) -> np.ndarray:
+    """xi = [phi_theta(x_1), ..., phi_theta(x_n)] in R_+^{r x n} with
+    phi_theta(x) = r^{-1/2} (phi(x,u_1), ..., phi(x,u_r)).  Direct
+    difference form, fp64: xi[k,i] = exp(-(2/eps) sum_c (x_ic-u_kc)^2 + |u_k|^2/(eps q)
+    + (d/4) ln 2q - (1/2) ln r)."""
+    X = np.asarray(X, dtype=np.float64)
+    U = np.asarray(U, dtype=np.float64)
+    r, d = U.shape
+    sq = np.zeros((r, X.shape[0]))
+    for c in range(d):
+        sq += (U[:, c][:, None] - X[:, c][None, :]) ** 2
+    uu = (U * U).sum(axis=1)
+    log_scale = 0.25 * d * math.log(2.0 * q) - 0.5 * math.log(r)
+    return np.exp(-2.0 / eps * sq + (uu / (eps * q))[:, None] + log_scale)
+
+
+def feature_entries_scaled(X: np.ndarray, U: np.ndarray, eps: float, q: float, r: int,
+                           rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """phi(x_i, u_k)/sqrt(r) for each sampled pair (rows[j], cols[j])."""
+    x = np.asarray(X, dtype=np.float64)[rows]
+    u = np.asarray(U, dtype=np.float64)[cols]
+    return gaussian_phi(x, u, eps, q) / math.sqrt(r)
+
+
+# ---------------------------------------------------------------------------------------
+# Alg. 1 Sinkhorn on a generic positive operator K
+# ---------------------------------------------------------------------------------------
+def sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
+             Kt_mv: Callable[[np.ndarray], np.ndarray],
+             a: np.ndarray, b: np.ndarray, T: Optional[int] = None,
+             tol: Optional[float] = None, max_iter: int = 100000,
+             record_err: bool = False) -> dict:
+    """Alg. 1: inputs K, a, b, delta, u.  u^0 = 1_n (reading C6).  Repeat
+    v <- b / K^T u ; u <- a / K v  until |v o K^T u - b|_1 < delta.
+
+    Fixed-T mode (tol None): exactly T iterations.  Tolerance mode: stop after the first
+    iteration t whose err_t = |v^t o K^T u^t - b|_1 < tol (checked every iteration).
+    Returns u, v, iters, errs (err_t per iteration when recorded), converged."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    u = np.ones(a.shape[0])
+    v = np.ones(b.shape[0])
+    errs = []
+    iters = 0
+    converged = False
+    n_iter = T if tol is None else max_iter
+    for _ in range(n_iter):
+        v = b / Kt_mv(u)
+        u = a / K_mv(v)
+        iters += 1
+        if tol is not None or record_err:
+            err = float(np.abs(v * Kt_mv(u) - b).sum())
+            errs.append(err)
+            if tol is not None and err < tol:
+                converged = True
+                break
+    return dict(u=u, v=v, iters=iters, errs=np.array(errs), converged=converged)
+
+
+def sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, T=None, tol=None,
+                      record_err=False, max_iter=100000) -> dict:
+    """Alg. 1 with K_theta = xi^T zeta: K v = xi^T (zeta v),
+    K^T u = zeta^T (xi u) — r(n+m) operations per application.
+    xi is r x n, zeta is r x m (paper layout)."""
+    xi = np.asarray(xi, dtype=np.float64)
+    zeta = np.asarray(zeta, dtype=np.float64)
+    return sinkhorn(lambda v: xi.T @ (zeta @ v), lambda u: zeta.T @ (xi @ u), a, b, T, tol,
+                    max_iter, record_err)
+
+
+def sinkhorn_dense(K: np.ndarray, a, b, T=None, tol=None, record_err=False,
+                   max_iter=100000) -> dict:
+    """Alg. 1 on an explicitly stored n x m kernel (2nm operations)."""
+    K = np.asarray(K, dtype=np.float64)
+    return sinkhorn(lambda v: K @ v, lambda u: K.T @ u, a, b, T, tol, max_iter, record_err)
+
+
+# ---------------------------------------------------------------------------------------
+# a9. Dual estimate and primal objective
+# ---------------------------------------------------------------------------------------
+def dual_estimate(u, v, a, b, eps: float) -> float:
+    """W_hat = eps (a^T log u + b^T log v)  (eq. dual-estimate).  No separate
+    +eps: the -eps u^T K v + eps pair cancels because u^T K v = 1 after one loop
+    (reading C7)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(eps * (a @ np.log(u) + b @ np.log(v)))
+
+
+def primal_objective(P: np.ndarray, C: np.ndarray, eps: float) -> float:
+    """<P, C> - eps H(P) + eps with H(P) = -sum P (log P - 1)."""
+    H = -float((P * (np.log(P) - 1.0)).sum())
+    return float((P * C).sum()) - eps * H + eps
+
+
+def gaussian_kernel_dense(X, Y, eps: float) -> np.ndarray:
+    """k(x,y) = exp(-|x-y|^2 / eps)  (Lemma decomp-RBF statement)."""
+    X = np.asarray(X, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    sq = (X * X).sum(1)[:, None] + (Y * Y).sum(1)[None, :] - 2.0 * X @ Y.T
+    sq = np.maximum(sq, 0.0)
+    return np.exp(-sq / eps)
+
+
+def marginal_error(u, v, Kt_u, b) -> float:
+    """|v o K^T u - b|_1 (stopping criterion of Alg. 1)."""
+    return float(np.abs(v * Kt_u - np.asarray(b, dtype=np.float64)).sum())
+
+
+# ---------------------------------------------------------------------------------------
+# The whole hot path, in paper order: a1 -> a2 -> a3 -> Alg. 1 -> a9
+# ---------------------------------------------------------------------------------------
+def rot(X, Y, a, b, eps: float, r: int, seed: int, T: Optional[int] = None,
+        tol: Optional[float] = None, R: Optional[float] = None, record_err=False,
+        U: Optional[np.ndarray] = None) -> dict:
+    """W_hat_{eps,c_theta}(mu, nu) for mu = sum a_i delta_{x_i}, nu = sum b_j delta_{y_j}
+    (problem statement PAPER.md:220-222), computed by Alg. 1 on K_theta = xi^T zeta."""
+    d = np.asarray(X).shape[1]
+    if R is None:
+        R = max_norm(X, Y)
+    prm = gaussian_params(eps, d, r, R)
+    if U is None:
+        U = draw_anchors(r, d, prm["sigma"], seed)
+    xi = feature_matrix(X, U, eps, prm["q"])
+    zeta = feature_matrix(Y, U, eps, prm["q"])
+    sol = sinkhorn_factored(xi, zeta, a, b, T=T, tol=tol, record_err=record_err)
+    sol.update(rot=dual_estimate(sol["u"], sol["v"], a, b, eps), U=U, xi=xi, zeta=zeta,
+               params=prm)
+    return sol
