@@ -1,0 +1,195 @@
+/*
+ * lsk.h — C ABI of the B200 (sm_100a) linear-time Sinkhorn library ("lsk").
+ *
+ * Method: arXiv 2006.07057, "Linear Time Sinkhorn Divergences using Positive Features".
+ * PAPER.md line numbers refer to /root/reference/PAPER.md (full paper = lines 181-1162).
+ *
+ *   mu = sum_i a_i delta_{x_i},  nu = sum_j b_j delta_{y_j},  eps > 0
+ *   phi(x,u) = (2q)^{d/4} exp(-2|x-u|^2/eps) exp(|u|^2/(eps q))
+ *   phi_theta(x) = r^{-1/2} (phi(x,u_1), ..., phi(x,u_r)),  u_k ~ N(0, q eps/4 I)
+ *
+ *   K_theta = xi zeta^T with xi in R_+^{n x r}, zeta in R_+^{m x r}    (
+ *             the paper stores xi as r x n, we store its transpose — reading C9)
+ *   Alg. 1: u^0 = 1; repeat v <- b / K^T u ; u <- a / K v
+ *   W_hat  = eps (a^T log u + b^T log v)
+ *
+ * Conventions (all entry points):
+ *   - Every array argument is a caller-owned, contiguous, row-major DEVICE pointer (e.g.
+ *     from a torch CUDA tensor) unless the parameter name ends in _host; fp32 unless noted;
+ *     16-byte aligned.  Inputs are never modified.  The library owns only an internal
+ *     workspace cached per (device, stream): fp64 CTA partials, r-vectors, barrier
+ *     counters, a second v buffer and a result block.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous, EXCEPT: lsk_feature_params_init with R <= 0, any call
+ *     given a non-NULL host `lsk_report*`/`double*` result, and lsk_rot_host — these
+ *     synchronise `stream` before returning.
+ *   - Errors: a negative lsk_status; lsk_last_error() returns a thread-local message.  No
+ *     C++ exception crosses the ABI.  On error, outputs are unspecified.
+ *   - Thread safety: calls on different streams may run concurrently; one solve at a time
+ *     per (device, stream) workspace.
+ */
+#ifndef LSK_H
+#define LSK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum lsk_status {
+  LSK_OK = 0,
+  LSK_NOT_CONVERGED = 1,   /* warning: tol > 0 and max_iters reached; outputs valid        */
+  LSK_EINVAL = -1,         /* n,m,r,d < 1; eps <= 0; r % 4 != 0; NULL or misaligned pointer */
+  LSK_EDIM = -2,           /* unsupported size combination (e.g. d > 16 for implicit)       */
+  LSK_EDOMAIN = -3,        /* R given and a point lies outside B(0,R); W0 argument < -1/e   */
+  LSK_EWEIGHTS = -4,       /* reserved: weight validation failure                           */
+  LSK_EBREAKDOWN = -5,     /* a row dot K v or K^T u was 0 / inf / nan        */
+  LSK_ECUDA = -6,          /* CUDA runtime error (message in lsk_last_error)                 */
+  LSK_ENCCL = -7,          /* NCCL error or NCCL library not loadable                       */
+  LSK_ENOMEM = -8,         /* workspace allocation failed                                   */
+  LSK_EUNSUPPORTED = -9    /* e.g. cooperative launch unavailable                           */
+} lsk_status;
+
+/* Gaussian positive-feature parameters (Lemma decomp-RBF).
+ *   z = R^2/(eps d), q = z / (2 W_0(z)), sigma = sqrt(q eps / 4),
+ *   log_scale = (d/4) ln(2q) - (1/2) ln r.   All fp64, computed on the host. */
+typedef struct lsk_feature_params {
+  double eps;
+  double R;
+  double q;
+  double sigma;
+  double log_scale;
+  int32_t d;
+  int32_t r;
+  uint64_t seed;
+} lsk_feature_params;
+
+/* Solve options.  tol <= 0: run exactly max_iters iterations (fixed-T mode).  tol > 0:
+ * stop after the first iteration t with |v^t o K^T u^t - b|_1 < tol, at most
+ * max_iters.  want_marginal_err (fixed-T mode): also evaluate |v^T o K^T u^T - b|_1 with
+ * one extra half pass.  variant (implicit solver only): 0 = auto. */
+typedef struct lsk_solve_opts {
+  int32_t max_iters;
+  int32_t want_marginal_err;
+  double tol;
+  int32_t ctas_per_sm;     /* 0 = library default                                         */
+  int32_t reserved;
+} lsk_solve_opts;
+
+/* Report of one solve.  rot = W_hat of the returned (u, v);
+ * marginal_err = |v o K^T u - b|_1 of the returned state, or -1 if not evaluated. */
+typedef struct lsk_report {
+  int32_t iters;
+  int32_t converged;
+  double marginal_err;
+  double rot;
+  double sum_a_log_u;      /* a^T log u (fp64)                                            */
+  double sum_b_log_v;      /* b^T log v (fp64)                                            */
+  int32_t breakdown;       /* 1 if a zero / non-finite row dot was seen                   */
+  int32_t reserved;
+} lsk_report;
+
+typedef struct lsk_comm lsk_comm;   /* opaque NCCL communicator; NULL = single GPU */
+
+const char* lsk_version(void);
+const char* lsk_last_error(void);
+
+/* ---- a1: feature parameters (host fp64) --------------------------------------------- */
+/* Principal-branch Lambert W_0 ("W_0 is the Lambert function"); Halley
+ * iteration from log1p(z).  z < -1/e -> LSK_EDOMAIN.  Host only, no GPU needed. */
+lsk_status lsk_lambert_w0(double z, double* w);
+
+/* Fills *out from (eps, d, r, R, seed).  R <= 0: R = max(max_i |x_i|, max_j |y_j|)
+ * computed on the device from X (n x d) and Y (m x d) in fp64 (reading C3; synchronises).
+ * R > 0: X/Y may be NULL; if given, a point with |p| > R gives LSK_EDOMAIN.
+ * With a communicator, the auto-R max is all-reduced across ranks. */
+lsk_status lsk_feature_params_init(double eps, int32_t d, int32_t r, double R, uint64_t seed,
+                                   const float* X, int64_t n, const float* Y, int64_t m,
+                                   lsk_feature_params* out, lsk_comm* comm, void* stream);
+
+/* ---- a2: anchors theta = (u_1..u_r), u_k ~ N(0, sigma^2 I) ---- */
+/* U (r x d, fp32, device) = fp32(sigma * z_kc); z from Philox4x32-10 with
+ * key = (seed & 0xffffffff, seed >> 32), counter = (k, c/4, 0, 0), fp64 Box-Muller on word
+ * pairs (w0,w1) and (w2,w3): z = sqrt(-2 ln((w0+1) 2^-32)) (cos, sin)(2 pi w1 2^-32)
+ * (reading C5).  Prefix property: anchor k does not depend on r. */
+lsk_status lsk_draw_anchors(const lsk_feature_params* p, float* U, void* stream);
+/* Raw generator words, for bit-exact testing: out (device uint32, r x ceil(d/4) x 4). */
+lsk_status lsk_philox_words(uint64_t seed, int32_t r, int32_t d, uint32_t* out, void* stream);
+
+/* ---- a3: feature map xi = phi_theta(X) --------------------- */
+/* Xi (n x r, fp32, device): Xi[i][k] = exp(-(2/eps)|x_i - U_k|^2 + |U_k|^2/(eps q)
+ *   + log_scale).  d <= 16: direct difference form on FFMA; d > 16: expanded form
+ * |x|^2 + |U|^2 - 2 x.U with the contraction tiled through shared memory. r % 4 == 0. */
+lsk_status lsk_feature_map(const lsk_feature_params* p, const float* U, const float* X,
+                           int64_t n, float* Xi, void* stream);
+/* Batched: X is (batch, n, d), Xi is (batch, n, r); one shared anchor draw (config 4). */
+lsk_status lsk_feature_map_batched(const lsk_feature_params* p, const float* U,
+                                   const float* X, int64_t n, int32_t batch, float* Xi,
+                                   void* stream);
+
+/* ---- a4-a9: Alg. 1 on K_theta = Xi Zeta^T, streaming the factors from HBM ---------- */
+/* One persistent launch runs every iteration: per iteration a zeta-pass
+ * (t_j = zeta_j . s_v, v_j = b_j / t_j, s_u += v_j zeta_j) and a xi-pass (mirror), each
+ * reading its factor once (4 r (n+m) bytes / iteration); r-vectors reduced in fp64 across
+ * CTAs in a fixed order (deterministic).  u^0 = 1 (reading C6).  u (n), v (m) outputs.
+ * rep (host, nullable): if non-NULL the call synchronises and fills it.
+ * comm: rows are sharded by the caller (n, m, Xi, Zeta, a, b, u, v are LOCAL shards; r and
+ * eps global); one fp64 all-reduce of r+4 doubles per half iteration. */
+lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                 int32_t r, const float* a, const float* b, double eps,
+                                 const lsk_solve_opts* o, float* u, float* v,
+                                 lsk_report* rep, lsk_comm* comm, void* stream);
+
+/* Same iteration, but xi/zeta entries are regenerated in registers from (X, Y, U) in every
+ * pass and never stored (MUFU ex2 per entry per pass).  d <= 16. */
+lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const float* U,
+                                          const float* X, int64_t n, const float* Y,
+                                          int64_t m, const float* a, const float* b,
+                                          const lsk_solve_opts* o, float* u, float* v,
+                                          lsk_report* rep, lsk_comm* comm, void* stream);
+
+/* Batched: `batch` independent problems in ONE launch, one CTA (no grid barrier) per
+ * problem.  Xi (batch, n, r), Zeta (batch, m, r), a/u (batch, n), b/v (batch, m);
+ * reps: host array of `batch` reports (nullable). */
+lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float* Zeta,
+                                         int64_t m, int32_t r, int32_t batch, const float* a,
+                                         const float* b, double eps, const lsk_solve_opts* o,
+                                         float* u, float* v, lsk_report* reps, void* stream);
+
+/* ---- a9: read-out W_hat = eps (a^T log u + b^T log v) in fp64 ------- */
+/* rot_host: host double (the call synchronises).  With comm, partial sums are all-reduced. */
+lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,
+                         int64_t n, int64_t m, double eps, double* rot_host, lsk_comm* comm,
+                         void* stream);
+lsk_status lsk_rot_value_batched(const float* u, const float* v, const float* a,
+                                 const float* b, int64_t n, int64_t m, int32_t batch,
+                                 double eps, double* rots_host, void* stream);
+
+/* ---- whole path with HOST buffers (end-to-end entry point) ---------------------------- */
+/* X_host (n x d), Y_host (m x d), a_host, b_host (host memory, pinned or pageable).  Copies
+ * inputs to the device, runs a1-a9 (variant 0 = auto, 1 = streaming, 2 = implicit), copies
+ * u, v (nullable) and the report back.  Synchronous. */
+lsk_status lsk_rot_host(const float* X_host, int64_t n, const float* Y_host, int64_t m,
+                        int32_t d, const float* a_host, const float* b_host, double eps,
+                        int32_t r, uint64_t seed, double R, const lsk_solve_opts* o,
+                        int32_t variant, float* u_host, float* v_host, lsk_report* rep);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) -------------------------------- */
+/* Row shard [begin, end) of `total` rows for `rank` of `nranks` (contiguous, balanced). */
+lsk_status lsk_shard_range(int64_t total, int32_t nranks, int32_t rank, int64_t* begin,
+                           int64_t* end);
+/* 128-byte ncclUniqueId into out_host (rank 0 creates it; broadcast it yourself). */
+lsk_status lsk_comm_get_unique_id(void* out_host);
+lsk_status lsk_comm_init(lsk_comm** out, int32_t nranks, int32_t rank,
+                         const void* unique_id_host, int32_t device);
+lsk_status lsk_comm_destroy(lsk_comm* comm);
+
+/* Number of kernels the library launched on this thread since the last reset (for the
+ * bench's gpu_launches claim). */
+int64_t lsk_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSK_H */

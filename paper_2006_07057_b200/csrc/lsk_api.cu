@@ -1,0 +1,668 @@
+// lsk_api.cu — host side of the C ABI declared in include/lsk.h: validation, fp64 feature
+// parameters (Lambert W_0), workspace cache, launch configuration, NCCL (dlopen'ed) and the
+// host-buffer end-to-end entry point.  No torch types anywhere.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "lsk_internal.h"
+
+namespace lsk {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+void count_launch(int k) { g_launches += k; }
+
+static lsk_status fail(lsk_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+#define LSK_CU(call)                                                                      \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(LSK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+#define LSK_TRY(call)                 \
+  do {                                \
+    lsk_status st_ = (call);          \
+    if (st_ < 0) return st_;          \
+  } while (0)
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ device properties ---
+static int num_sms() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = v > 0 ? v : 1;
+  return cache[dev];
+}
+static int max_smem_optin() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+// ------------------------------------------------------------------ workspace cache -----
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+static lsk_status get_ws(cudaStream_t s, size_t bytes, char** out) {
+  int dev = 0;
+  LSK_CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& w = g_ws[{dev, s}];
+  if (w.bytes < bytes) {
+    if (w.ptr) {
+      cudaStreamSynchronize(s);
+      cudaFree(w.ptr);
+      w.ptr = nullptr;
+      w.bytes = 0;
+    }
+    const size_t nb = bytes + bytes / 4 + (1u << 20);
+    if (cudaMalloc(&w.ptr, nb) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LSK_ENOMEM, "workspace cudaMalloc failed");
+    }
+    w.bytes = nb;
+  }
+  *out = static_cast<char*>(w.ptr);
+  return LSK_OK;
+}
+
+struct Carve {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+// ------------------------------------------------------------------ NCCL (dlopen) -------
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOLOAD | RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* env = getenv("LSK_NCCL_PATH");
+      if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
+  });
+  return api;
+}
+
+}  // namespace lsk
+
+struct lsk_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1;
+  int rank = 0;
+  int device = 0;
+};
+
+namespace lsk {
+
+static lsk_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return LSK_OK;
+  const char* s = nccl().errStr ? nccl().errStr(r) : "?";
+  return fail(LSK_ENCCL, std::string(what) + ": " + s);
+}
+
+// ------------------------------------------------------------------ Lambert W_0 ---------
+static lsk_status lambert_w0(double z, double* w) {
+  if (!(z >= -1.0 / M_E)) return fail(LSK_EDOMAIN, "lambert_w0: argument < -1/e");
+  if (z == 0.0) {
+    *w = 0.0;
+    return LSK_OK;
+  }
+  double x = z > 0 ? std::log1p(z) : -0.5;
+  for (int it = 0; it < 100; ++it) {
+    const double ex = std::exp(x);
+    const double f = x * ex - z;
+    const double xp1 = x + 1.0;
+    const double step = f / (ex * xp1 - (x + 2.0) * f / (2.0 * xp1));
+    x -= step;
+    if (std::fabs(step) <= 1e-15 * (1.0 + std::fabs(x))) break;
+  }
+  *w = x;
+  return LSK_OK;
+}
+
+// ------------------------------------------------------------------ Sinkhorn driver -----
+struct SolveCfg {
+  bool impl = false;
+  int batch = 1;
+  int gpp = 1;
+  int grid = 1;
+  size_t smem = 0;
+  int nstage = 2;
+  int stage_floats = 0;
+  bool coop = false;
+};
+
+static lsk_status plan_solve(const SinkArgs& A, bool impl, int batch, const lsk_solve_opts* o,
+                             SolveCfg* c) {
+  int tr, nv;
+  sinkhorn_tile_config(A.r, impl, &tr, &nv);
+  if (nv > (impl ? 4 : 8)) return fail(LSK_EDIM, "r too large for this variant");
+  c->impl = impl;
+  c->batch = batch;
+  const int hdr = 64 + 32 * 16;
+  int sf = hdr + (impl ? 0 : tr * A.r);
+  sf = (sf + 31) & ~31;
+  c->stage_floats = sf;
+  int cps = (o && o->ctas_per_sm > 0) ? o->ctas_per_sm : (impl ? 2 : (batch > 1 ? 2 : 1));
+  const size_t static_smem = sinkhorn_static_smem();
+  const size_t smem_sm = 227 * 1024;   // B200: 228 KB per SM, 227 KB usable per CTA
+  const size_t per_cta = std::min<size_t>(max_smem_optin(), smem_sm / cps - 1024);
+  const size_t stage_bytes = (size_t)sf * 4;
+  int nst = (int)((per_cta - static_smem - 512) / stage_bytes);
+  nst = std::min(nst, impl ? 8 : 16);
+  if (nst < 2) {
+    cps = 1;
+    nst = (int)((std::min<size_t>(max_smem_optin(), smem_sm) - static_smem - 512) / stage_bytes);
+    nst = std::min(nst, 16);
+    if (nst < 2) return fail(LSK_EDIM, "r too large: two ring stages do not fit in shared memory");
+  }
+  c->nstage = nst;
+  c->smem = (size_t)nst * stage_bytes;
+  int occ = sinkhorn_max_ctas_per_sm(impl, A.r, A.d, c->smem);
+  if (occ < 1) return fail(LSK_EUNSUPPORTED, "sinkhorn kernel does not fit on an SM");
+  cps = std::min(cps, occ);
+  const int sms = num_sms();
+  if (batch > 1) {
+    c->gpp = 1;
+    c->grid = batch;
+    c->coop = false;
+  } else {
+    const int64_t rows = std::max(A.rows[0], A.rows[1]);
+    const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
+    c->gpp = (int)std::min<int64_t>((int64_t)sms * cps, want);
+    c->grid = c->gpp;
+    c->coop = c->gpp > 1;
+  }
+  return LSK_OK;
+}
+
+static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_opts* o,
+                            lsk_report* reps, lsk_comm* comm, cudaStream_t s, char* ws,
+                            Carve& cv) {
+  if (!o) return fail(LSK_EINVAL, "opts is NULL");
+  if (o->max_iters < 1) return fail(LSK_EINVAL, "max_iters < 1");
+  A.T = o->max_iters;
+  A.tol_mode = o->tol > 0.0 ? 1 : 0;
+  A.tol = o->tol;
+  A.want_err = (A.tol_mode || o->want_marginal_err) ? 1 : 0;
+  A.num_passes = 2 * A.T + 1 + A.want_err;
+  SolveCfg c;
+  LSK_TRY(plan_solve(A, impl, batch, o, &c));
+  if (comm && c.gpp < 2) {
+    // the multi-launch path needs svec: force >= 2 CTAs
+    c.gpp = std::min(2, num_sms());
+    c.grid = c.gpp;
+    c.coop = true;
+  }
+  A.gpp = c.gpp;
+  A.nprob = batch;
+  A.nstage = c.nstage;
+  A.stage_floats = c.stage_floats;
+  const int64_t rs = A.r + kExtra;
+  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * rs * c.gpp * batch));
+  A.svec = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * rs * batch));
+  A.state = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * kStateDoubles * batch));
+  A.bar = reinterpret_cast<unsigned int*>(ws + cv.take(sizeof(unsigned int) * batch));
+  A.vbuf1 = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * A.rows[1] * batch));
+  LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles * batch, s));
+  if (!comm) {
+    A.pass_begin = 0;
+    A.pass_end = A.num_passes;
+    A.multi_launch = 0;
+    LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
+    LSK_CU(launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+  } else {
+    if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
+    A.multi_launch = 1;
+    for (int p = 0; p <= A.num_passes; ++p) {
+      A.pass_begin = p;
+      A.pass_end = std::min(p + 1, A.num_passes);
+      if (p == A.num_passes) A.pass_end = p;   // finalise-only launch
+      LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
+      LSK_CU(launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+      if (p < A.num_passes)
+        LSK_TRY(nccl_check(nccl().allReduce(A.svec, A.svec, (size_t)rs * batch, ncclFloat64,
+                                            ncclSum, comm->comm, s),
+                           "ncclAllReduce"));
+    }
+  }
+  if (reps) {
+    std::vector<double> st((size_t)kStateDoubles * batch);
+    LSK_CU(cudaMemcpyAsync(st.data(), A.state, sizeof(double) * st.size(), cudaMemcpyDeviceToHost, s));
+    LSK_CU(cudaStreamSynchronize(s));
+    bool brk = false, notconv = false;
+    for (int b = 0; b < batch; ++b) {
+      const double* x = st.data() + (size_t)b * kStateDoubles;
+      lsk_report& rp = reps[b];
+      rp.iters = (int32_t)x[ST_ITERS];
+      rp.converged = (int32_t)x[ST_CONV];
+      rp.marginal_err = x[ST_ERR];
+      rp.rot = x[ST_ROT];
+      rp.sum_a_log_u = x[ST_FINAL_A];
+      rp.sum_b_log_v = x[ST_FINAL_B];
+      rp.breakdown = x[ST_BRK] > 0 ? 1 : 0;
+      rp.reserved = 0;
+      brk |= rp.breakdown != 0;
+      notconv |= A.tol_mode && !rp.converged;
+    }
+    if (brk) return fail(LSK_EBREAKDOWN, "zero or non-finite row dot during Sinkhorn");
+    if (notconv) {
+      g_err = "tolerance not reached within max_iters";
+      return LSK_NOT_CONVERGED;
+    }
+  }
+  return LSK_OK;
+}
+
+static size_t solve_ws_bytes(int r, int64_t m, int batch, int gpp_max) {
+  const int64_t rs = r + kExtra;
+  return 256 * 8 + sizeof(double) * rs * gpp_max * batch + sizeof(double) * rs * batch +
+         sizeof(double) * kStateDoubles * batch + sizeof(unsigned) * batch +
+         sizeof(float) * m * batch;
+}
+
+static lsk_status check_common(int64_t n, int64_t m, int r, double eps) {
+  if (n < 1 || m < 1) return fail(LSK_EINVAL, "n and m must be >= 1");
+  if (r < 1 || (r % 4) != 0) return fail(LSK_EINVAL, "r must be >= 1 and a multiple of 4");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(LSK_EINVAL, "eps must be > 0");
+  if (n > (int64_t)1 << 40 || m > (int64_t)1 << 40) return fail(LSK_EINVAL, "n or m too large");
+  return LSK_OK;
+}
+
+}  // namespace lsk
+
+using namespace lsk;
+
+// ========================================================================================
+extern "C" {
+
+const char* lsk_version(void) { return "lsk 0.1.0 (sm_100a)"; }
+const char* lsk_last_error(void) { return g_err.c_str(); }
+int64_t lsk_launch_count(int32_t reset) {
+  const int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+lsk_status lsk_lambert_w0(double z, double* w) {
+  if (!w) return fail(LSK_EINVAL, "w is NULL");
+  return lambert_w0(z, w);
+}
+
+lsk_status lsk_shard_range(int64_t total, int32_t nranks, int32_t rank, int64_t* begin,
+                           int64_t* end) {
+  if (!begin || !end || nranks < 1 || rank < 0 || rank >= nranks || total < 0)
+    return fail(LSK_EINVAL, "bad shard arguments");
+  *begin = total * rank / nranks;
+  *end = total * (rank + 1) / nranks;
+  return LSK_OK;
+}
+
+lsk_status lsk_feature_params_init(double eps, int32_t d, int32_t r, double R, uint64_t seed,
+                                   const float* X, int64_t n, const float* Y, int64_t m,
+                                   lsk_feature_params* out, lsk_comm* comm, void* stream) {
+  if (!out) return fail(LSK_EINVAL, "out is NULL");
+  if (d < 1 || r < 1) return fail(LSK_EINVAL, "d and r must be >= 1");
+  if (!(eps > 0.0)) return fail(LSK_EINVAL, "eps must be > 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool have_pts = (X && n > 0) || (Y && m > 0);
+  double maxnorm = -1.0;
+  if (have_pts) {
+    char* ws;
+    LSK_TRY(get_ws(s, 4096, &ws));
+    unsigned long long* dmax = reinterpret_cast<unsigned long long*>(ws);
+    LSK_CU(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s));
+    if (X && n > 0) LSK_CU(launch_max_sqnorm(X, n, d, dmax, s));
+    if (Y && m > 0) LSK_CU(launch_max_sqnorm(Y, m, d, dmax, s));
+    if (comm) {
+      if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
+      LSK_TRY(nccl_check(nccl().allReduce(dmax, dmax, 1, ncclUint64, ncclMax, comm->comm, s),
+                         "ncclAllReduce(max)"));
+    }
+    unsigned long long hbits = 0;
+    LSK_CU(cudaMemcpyAsync(&hbits, dmax, sizeof(hbits), cudaMemcpyDeviceToHost, s));
+    LSK_CU(cudaStreamSynchronize(s));
+    double sq;
+    std::memcpy(&sq, &hbits, sizeof(sq));
+    maxnorm = std::sqrt(sq);
+  }
+  if (R <= 0.0) {
+    if (!have_pts) return fail(LSK_EINVAL, "R <= 0 requires X or Y to compute R");
+    R = maxnorm;
+    if (!(R > 0.0)) R = 1e-30;   // all points at the origin: any R works (C11)
+  } else if (have_pts && maxnorm > R * (1.0 + 1e-12)) {
+    return fail(LSK_EDOMAIN, "a point lies outside B(0,R)");
+  }
+  const double z = R * R / (eps * d);
+  double W;
+  LSK_TRY(lambert_w0(z, &W));
+  const double q = (W > 0.0) ? z / (2.0 * W) : 0.5;   // z -> 0: q -> 1/2
+  out->eps = eps;
+  out->R = R;
+  out->q = q;
+  out->sigma = std::sqrt(q * eps / 4.0);
+  out->log_scale = 0.25 * d * std::log(2.0 * q) - 0.5 * std::log((double)r);
+  out->d = d;
+  out->r = r;
+  out->seed = seed;
+  return LSK_OK;
+}
+
+lsk_status lsk_draw_anchors(const lsk_feature_params* p, float* U, void* stream) {
+  if (!p || !U) return fail(LSK_EINVAL, "NULL argument");
+  if (p->r < 1 || p->d < 1) return fail(LSK_EINVAL, "bad params");
+  LSK_CU(launch_anchors(p->seed, p->r, p->d, p->sigma, U, nullptr, static_cast<cudaStream_t>(stream)));
+  return LSK_OK;
+}
+
+lsk_status lsk_philox_words(uint64_t seed, int32_t r, int32_t d, uint32_t* out, void* stream) {
+  if (!out || r < 1 || d < 1) return fail(LSK_EINVAL, "bad arguments");
+  LSK_CU(launch_anchors(seed, r, d, 0.0, nullptr, out, static_cast<cudaStream_t>(stream)));
+  return LSK_OK;
+}
+
+static lsk_status feature_map_impl(const lsk_feature_params* p, const float* U, const float* X,
+                                   int64_t rows, float* Xi, cudaStream_t s) {
+  if (!p || !U || !X || !Xi) return fail(LSK_EINVAL, "NULL argument");
+  if (p->r < 4 || p->r % 4) return fail(LSK_EINVAL, "r must be a multiple of 4");
+  if (rows < 1) return fail(LSK_EINVAL, "n must be >= 1");
+  if (!aligned16(Xi)) return fail(LSK_EINVAL, "Xi must be 16-byte aligned");
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  const size_t oD = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  float* bD = reinterpret_cast<float*>(ws + oD);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, bD, s));
+  LSK_CU(launch_feature_map(X, rows, p->d, U, Wt, b2, bD, p->r, p->eps, Xi, s));
+  return LSK_OK;
+}
+
+lsk_status lsk_feature_map(const lsk_feature_params* p, const float* U, const float* X,
+                           int64_t n, float* Xi, void* stream) {
+  return feature_map_impl(p, U, X, n, Xi, static_cast<cudaStream_t>(stream));
+}
+
+lsk_status lsk_feature_map_batched(const lsk_feature_params* p, const float* U, const float* X,
+                                   int64_t n, int32_t batch, float* Xi, void* stream) {
+  if (batch < 1) return fail(LSK_EINVAL, "batch must be >= 1");
+  // one shared anchor draw: the batch is a (batch*n) x d point matrix
+  return feature_map_impl(p, U, X, n * batch, Xi, static_cast<cudaStream_t>(stream));
+}
+
+lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                 int32_t r, const float* a, const float* b, double eps,
+                                 const lsk_solve_opts* o, float* u, float* v, lsk_report* rep,
+                                 lsk_comm* comm, void* stream) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (!Xi || !Zeta || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SinkArgs A{};
+  A.F[0] = Xi; A.F[1] = Zeta;
+  A.rows[0] = n; A.rows[1] = m;
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.r = r; A.d = 1; A.eps = eps;
+  char* ws;
+  LSK_TRY(get_ws(s, solve_ws_bytes(r, m, 1, 2 * num_sms()), &ws));
+  Carve cv;
+  return run_solve(A, false, 1, o, rep, comm, s, ws, cv);
+}
+
+lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const float* U,
+                                          const float* X, int64_t n, const float* Y, int64_t m,
+                                          const float* a, const float* b,
+                                          const lsk_solve_opts* o, float* u, float* v,
+                                          lsk_report* rep, lsk_comm* comm, void* stream) {
+  if (!p) return fail(LSK_EINVAL, "params NULL");
+  LSK_TRY(check_common(n, m, p->r, p->eps));
+  if (!U || !X || !Y || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms()), &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  SinkArgs A{};
+  A.X[0] = X; A.X[1] = Y;
+  A.rows[0] = n; A.rows[1] = m;
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.r = p->r; A.d = p->d; A.eps = p->eps;
+  A.Wt = Wt; A.beta2 = b2;
+  A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
+  return run_solve(A, true, 1, o, rep, comm, s, ws, cv);
+}
+
+lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float* Zeta,
+                                         int64_t m, int32_t r, int32_t batch, const float* a,
+                                         const float* b, double eps, const lsk_solve_opts* o,
+                                         float* u, float* v, lsk_report* reps, void* stream) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (batch < 1) return fail(LSK_EINVAL, "batch must be >= 1");
+  if (!Xi || !Zeta || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SinkArgs A{};
+  A.F[0] = Xi; A.F[1] = Zeta;
+  A.rows[0] = n; A.rows[1] = m;
+  A.fstride[0] = n * r; A.fstride[1] = m * r;
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.wstride[0] = n; A.wstride[1] = m;
+  A.r = r; A.d = 1; A.eps = eps;
+  char* ws;
+  LSK_TRY(get_ws(s, solve_ws_bytes(r, m, batch, 1), &ws));
+  Carve cv;
+  if (batch == 1) return run_solve(A, false, 1, o, reps, nullptr, s, ws, cv);
+  return run_solve(A, false, batch, o, reps, nullptr, s, ws, cv);
+}
+
+lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,
+                         int64_t n, int64_t m, double eps, double* rot_host, lsk_comm* comm,
+                         void* stream) {
+  if (!u || !v || !a || !b || !rot_host) return fail(LSK_EINVAL, "NULL argument");
+  if (n < 1 || m < 1 || !(eps > 0)) return fail(LSK_EINVAL, "bad sizes or eps");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  LSK_TRY(get_ws(s, 8192 + 2 * 64 * sizeof(double), &ws));
+  double* part = reinterpret_cast<double*>(ws + 256);
+  double* out2 = reinterpret_cast<double*>(ws);
+  LSK_CU(launch_rot_value(u, v, a, b, n, m, 1, part, out2, s));
+  if (comm) {
+    if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
+    LSK_TRY(nccl_check(nccl().allReduce(out2, out2, 2, ncclFloat64, ncclSum, comm->comm, s),
+                       "ncclAllReduce(rot)"));
+  }
+  double h[2];
+  LSK_CU(cudaMemcpyAsync(h, out2, sizeof(h), cudaMemcpyDeviceToHost, s));
+  LSK_CU(cudaStreamSynchronize(s));
+  *rot_host = eps * (h[0] + h[1]);
+  return LSK_OK;
+}
+
+lsk_status lsk_rot_value_batched(const float* u, const float* v, const float* a,
+                                 const float* b, int64_t n, int64_t m, int32_t batch,
+                                 double eps, double* rots_host, void* stream) {
+  if (!u || !v || !a || !b || !rots_host) return fail(LSK_EINVAL, "NULL argument");
+  if (n < 1 || m < 1 || batch < 1 || !(eps > 0)) return fail(LSK_EINVAL, "bad sizes or eps");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  Carve cv;
+  const size_t oOut = cv.take(sizeof(double) * 2 * batch);
+  const size_t oPart = cv.take(sizeof(double) * 2 * 64 * batch);
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  double* out2 = reinterpret_cast<double*>(ws + oOut);
+  LSK_CU(launch_rot_value(u, v, a, b, n, m, batch, reinterpret_cast<double*>(ws + oPart), out2, s));
+  std::vector<double> h((size_t)2 * batch);
+  LSK_CU(cudaMemcpyAsync(h.data(), out2, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+  LSK_CU(cudaStreamSynchronize(s));
+  for (int i = 0; i < batch; ++i) rots_host[i] = eps * (h[2 * i] + h[2 * i + 1]);
+  return LSK_OK;
+}
+
+// ---------------------------------------------------------------- host-buffer pipeline --
+lsk_status lsk_rot_host(const float* X_host, int64_t n, const float* Y_host, int64_t m,
+                        int32_t d, const float* a_host, const float* b_host, double eps,
+                        int32_t r, uint64_t seed, double R, const lsk_solve_opts* o,
+                        int32_t variant, float* u_host, float* v_host, lsk_report* rep) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (!X_host || !Y_host || !a_host || !b_host || !o) return fail(LSK_EINVAL, "NULL argument");
+  if (d < 1) return fail(LSK_EINVAL, "d must be >= 1");
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  static std::map<int, std::pair<void*, size_t>> bufs;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  LSK_CU(cudaGetDevice(&dev));
+  if (!streams.count(dev)) {
+    cudaStream_t st;
+    LSK_CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    streams[dev] = st;
+  }
+  cudaStream_t s = streams[dev];
+  const bool impl = variant == 2 || (variant == 0 && d <= 8);
+  Carve cv;
+  const size_t oX = cv.take(sizeof(float) * n * d), oY = cv.take(sizeof(float) * m * d);
+  const size_t oa = cv.take(sizeof(float) * n), ob = cv.take(sizeof(float) * m);
+  const size_t ou = cv.take(sizeof(float) * n), ov = cv.take(sizeof(float) * m);
+  const size_t oU = cv.take(sizeof(float) * r * d);
+  const size_t oXi = impl ? 0 : cv.take(sizeof(float) * n * r);
+  const size_t oZe = impl ? 0 : cv.take(sizeof(float) * m * r);
+  auto& bb = bufs[dev];
+  if (bb.second < cv.off) {
+    if (bb.first) cudaFree(bb.first);
+    bb.first = nullptr;
+    bb.second = 0;
+    if (cudaMalloc(&bb.first, cv.off) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LSK_ENOMEM, "lsk_rot_host: device buffers do not fit");
+    }
+    bb.second = cv.off;
+  }
+  char* base = static_cast<char*>(bb.first);
+  float *X = (float*)(base + oX), *Y = (float*)(base + oY), *a = (float*)(base + oa),
+        *b = (float*)(base + ob), *u = (float*)(base + ou), *v = (float*)(base + ov),
+        *U = (float*)(base + oU);
+  LSK_CU(cudaMemcpyAsync(X, X_host, sizeof(float) * n * d, cudaMemcpyHostToDevice, s));
+  LSK_CU(cudaMemcpyAsync(Y, Y_host, sizeof(float) * m * d, cudaMemcpyHostToDevice, s));
+  LSK_CU(cudaMemcpyAsync(a, a_host, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+  LSK_CU(cudaMemcpyAsync(b, b_host, sizeof(float) * m, cudaMemcpyHostToDevice, s));
+  lsk_feature_params p;
+  LSK_TRY(lsk_feature_params_init(eps, d, r, R, seed, X, n, Y, m, &p, nullptr, s));
+  LSK_TRY(lsk_draw_anchors(&p, U, s));
+  lsk_report local{};
+  lsk_status st;
+  if (impl) {
+    st = lsk_factored_sinkhorn_implicit(&p, U, X, n, Y, m, a, b, o, u, v, &local, nullptr, s);
+  } else {
+    float* Xi = (float*)(base + oXi);
+    float* Ze = (float*)(base + oZe);
+    LSK_TRY(lsk_feature_map(&p, U, X, n, Xi, s));
+    LSK_TRY(lsk_feature_map(&p, U, Y, m, Ze, s));
+    st = lsk_factored_sinkhorn(Xi, n, Ze, m, r, a, b, eps, o, u, v, &local, nullptr, s);
+  }
+  if (st < 0) return st;
+  if (u_host) LSK_CU(cudaMemcpyAsync(u_host, u, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+  if (v_host) LSK_CU(cudaMemcpyAsync(v_host, v, sizeof(float) * m, cudaMemcpyDeviceToHost, s));
+  LSK_CU(cudaStreamSynchronize(s));
+  if (rep) *rep = local;
+  return st;
+}
+
+// ---------------------------------------------------------------- NCCL communicator -----
+lsk_status lsk_comm_get_unique_id(void* out_host) {
+  if (!out_host) return fail(LSK_EINVAL, "out is NULL");
+  if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
+  ncclUniqueId id;
+  LSK_TRY(nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId"));
+  std::memcpy(out_host, &id, sizeof(id));
+  return LSK_OK;
+}
+
+lsk_status lsk_comm_init(lsk_comm** out, int32_t nranks, int32_t rank,
+                         const void* unique_id_host, int32_t device) {
+  if (!out || !unique_id_host || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(LSK_EINVAL, "bad communicator arguments");
+  if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
+  LSK_CU(cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id_host, sizeof(id));
+  lsk_comm* c = new lsk_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  lsk_status st = nccl_check(nccl().commInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+  if (st < 0) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return LSK_OK;
+}
+
+lsk_status lsk_comm_destroy(lsk_comm* comm) {
+  if (!comm) return LSK_OK;
+  lsk_status st = LSK_OK;
+  if (comm->comm) st = nccl_check(nccl().commDestroy(comm->comm), "ncclCommDestroy");
+  delete comm;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// lsk_internal.h — internal interfaces between the host API (lsk_api.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lsk.h"
+
+namespace lsk {
+
+constexpr int kConsumerThreads = 256;              // 8 consumer warps per CTA
+constexpr int kThreads = kConsumerThreads + 32;    // + 1 producer warp
+constexpr int kExtra = 4;                          // extras appended to every r-vector:
+                                                   // [0]=err, [1]=slog, [2]=breakdown, [3]=0
+constexpr int kStateDoubles = 16;                  // per-problem solve state block
+// state block layout (doubles)
+enum StateIdx {
+  ST_A = 0,        // a^T log u of the latest u-pass
+  ST_B = 1,        // b^T log v of the latest v-pass
+  ST_BPREV = 2,    // b^T log v of the v-pass before it
+  ST_ERR = 3,      // latest marginal error
+  ST_STOP = 4,     // 1 once the solve has finished (early stop or last pass)
+  ST_ITERS = 5,    // iterations of the returned state
+  ST_ROT = 6,      // W_hat of the returned state
+  ST_CONV = 7,     // converged flag
+  ST_BRK = 8,      // breakdown count
+  ST_FINAL_A = 9,  // a^T log u of the returned state
+  ST_FINAL_B = 10  // b^T log v of the returned state
+};
+
+// Pass schedule: p = 0 init xi-pass (s_v = xi^T 1), p = 2t-1 v-pass of iteration t,
+// p = 2t u-pass of iteration t (t = 1..T), p = 2T+1 error pass (if requested).
+enum PassKind { PK_INIT = 0, PK_V = 1, PK_U = 2, PK_ERR = 3, PK_NONE = 4 };
+
+struct SinkArgs {
+  // factor 0 = xi side (rows n, weights a, output u); factor 1 = zeta side (m, b, v)
+  const float* F[2];       // streaming: feature matrices (rows x r)
+  const float* X[2];       // implicit: point matrices (rows x d)
+  int64_t rows[2];
+  int64_t fstride[2];      // per-problem element stride of F (or X) for batched
+  const float* w[2];       // a, b
+  float* out[2];           // u (user), v (user)
+  float* vbuf1;            // second v buffer (workspace)
+  int64_t wstride[2];      // per-problem stride of w / out / vbuf1 (elements)
+  int r;
+  int d;
+  int T;                   // max iterations
+  int want_err;            // append the error pass
+  int tol_mode;
+  double tol;
+  double eps;
+  int gpp;                 // CTAs per problem
+  int nprob;
+  int pass_begin;          // passes [pass_begin, pass_end) run in this launch
+  int pass_end;            // pass_end == num_passes also finalises
+  int num_passes;
+  int multi_launch;        // 1: one pass per launch (NCCL all-reduce of svec between launches)
+  int nstage;              // ring stages
+  int stage_floats;        // floats per stage (header + TR*r for streaming)
+  double* part;            // [nprob][(r+kExtra) * gpp] column-major partials
+  double* svec;            // [nprob][r+kExtra]
+  unsigned int* bar;       // [nprob] monotone barrier counters (zeroed once per solve)
+  double* state;           // [nprob][kStateDoubles]
+  // implicit-mode anchor data (fp32, r each; W is (d, r) column groups)
+  const float* Wt;         // [d][r]  W_kc = (4 log2e / eps) U_kc, transposed
+  const float* beta2;      // [r]     log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
+  float c2;                // -2 log2e / eps
+};
+
+// Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.
+cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool cooperative, int grid,
+                            size_t smem, cudaStream_t s);
+// Kernel configuration for a given r / mode: rows per tile and stage floats.
+void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv);
+size_t sinkhorn_static_smem();
+int sinkhorn_max_ctas_per_sm(bool implicit, int r, int d, size_t dyn_smem);
+
+// Feature kernels (lsk_features.cu)
+cudaError_t launch_max_sqnorm(const float* X, int64_t n, int d, unsigned long long* out,
+                              cudaStream_t s);
+cudaError_t launch_anchors(uint64_t seed, int r, int d, double sigma, float* U,
+                           uint32_t* words, cudaStream_t s);
+cudaError_t launch_anchor_prep(const float* U, int r, int d, double eps, double q,
+                               double log_scale, float* Wt, float* beta2, float* betaD,
+                               cudaStream_t s);
+cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
+                               const float* Wt, const float* beta2, const float* betaD, int r,
+                               double eps, float* Xi, cudaStream_t s);
+cudaError_t launch_rot_value(const float* u, const float* v, const float* a, const float* b,
+                             int64_t n, int64_t m, int batch, double* partials, double* out2,
+                             cudaStream_t s);
+
+// Launch counter (host, thread-local) used for the bench's gpu_launches claim.
+void count_launch(int k = 1);
+
+}  // namespace lsk

@@ -1,0 +1,629 @@
+// lsk_sinkhorn.cu — Alg. 1 on K_theta = xi zeta^T as ONE
+// persistent launch per solve (or one launch per pass when an NCCL all-reduce sits between
+// passes).
+//
+// Schedule ("row-fused passes"): an iteration is a v-pass over zeta then a u-pass over xi.
+// For each factor row j the pass computes t_j = F_j . s (fp32, r-long dot), w_j = c_j / t_j
+// (c = b for the v-pass, a for the u-pass), and accumulates s'_k += F_jk w_j — so each factor
+// is read from HBM exactly once per iteration: 4 r (n+m) bytes.  The
+// naive 4-GEMV schedule would read 8 r (n+m).
+//
+// CTA layout: 8 consumer warps + 1 producer warp.  The producer streams a contiguous row
+// range of the factor through a shared-memory ring with 1-D bulk async copies (TMA engine,
+// cp.async.bulk + mbarrier complete_tx) and fetches per-row scalars (c_j, v_old_j) with
+// cp.async; the factor stream does not depend on s, so the ring keeps HBM busy across the
+// grid barriers between passes.  Consumer thread t owns float4 column groups
+// {t, t+256, ...}: its slice of s and of the fp64 accumulator live in registers, so the
+// accumulation needs no intra-CTA reduction.  Row dots are reduced with a warp
+// transpose-reduce (TR rows in TR-1+5-log2(TR) shuffles) and one smem exchange.
+//
+// Precision (C13): r-long dots in fp32; the n-long accumulation of s in fp32 over
+// <= 32 rows, then fp64; cross-CTA reduction in fp64 in a fixed order (deterministic, no
+// float atomics).  Marginal error and a^T log u / b^T log v in fp64.
+//
+// Implicit variant (template IMPL): no factor in HBM — the producer stages point rows x_j
+// and the consumers regenerate F_jk = 2^(alpha2_j + beta2_k + sum_c W_kc x_jc) with MUFU
+// ex2 in registers (expanded form of PAPER.md:934 in base 2).
+#include <cmath>
+#include <cstdio>
+
+#include "lsk_internal.h"
+#include "lsk_ptx.cuh"
+
+namespace lsk {
+
+constexpr int NT = kConsumerThreads;
+constexpr int NW = NT / 32;
+constexpr int kHdr = 64 + 32 * 16;   // stage header floats: c[32], vold[32], x[32][16]
+constexpr int kMaxStages = 16;
+
+struct Smem {
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
+  float red[2][NW][32];
+  float vrow[2][32];
+  double xs[3][32];
+  double ext[kExtra];
+  int done_pass;
+  int stop;
+};
+
+__device__ __forceinline__ int pass_kind(int p, const SinkArgs& A) {
+  if (p == 0) return PK_INIT;
+  if (p <= 2 * A.T) return (p & 1) ? PK_V : PK_U;
+  if (p == 2 * A.T + 1 && A.want_err) return PK_ERR;
+  return PK_NONE;
+}
+
+__device__ __forceinline__ void cta_rows(int64_t total, int gpp, int cta, int64_t* r0,
+                                         int64_t* r1) {
+  *r0 = (total * cta) / gpp;
+  *r1 = (total * (cta + 1)) / gpp;
+}
+
+// Warp transpose-reduce: each lane holds v[0..TR) (one partial per row).  Returns, in every
+// lane, the warp total of row (lane >> (5 - log2 TR)).  Fixed shuffle pattern: deterministic.
+template <int TR>
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[TR], int lane) {
+#pragma unroll
+  for (int w = TR / 2, off = 16; w >= 1; w >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? v[i] : v[i + w];
+      const float keep = upper ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  constexpr int kLog = (TR >= 32) ? 5 : (TR >= 16) ? 4 : (TR >= 8) ? 3 : (TR >= 4) ? 2 : (TR >= 2) ? 1 : 0;
+#pragma unroll
+  for (int off = 16 >> kLog; off >= 1; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+  return v[0];
+}
+
+__device__ __forceinline__ double warp_sum_f64(double x) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+// Barrier among the gpp CTAs of one problem: monotone counter, k-th barrier waits for
+// k * gpp arrivals (counter zeroed once per solve by the host).
+__device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int target, int tid) {
+  named_bar(1, NT);
+  if (tid == 0) {
+    __threadfence();
+    red_release_add(ctr, 1u);
+    while (ld_acquire(ctr) < target) {
+    }
+    __threadfence();
+  }
+  named_bar(1, NT);
+}
+
+__device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
+  return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];
+}
+
+template <bool IMPL, int NV, int TR, int D>
+__global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A) {
+  extern __shared__ __align__(128) float ring[];
+  __shared__ Smem S;
+  constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;   // fp32 partial over <= 32 rows
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int prob = blockIdx.x / A.gpp;
+  const int cta = blockIdx.x - prob * A.gpp;
+  const int r = A.r;
+  double* stg_state = A.state + (int64_t)prob * kStateDoubles;
+
+  if (__ldcg(stg_state + ST_STOP) != 0.0) return;   // solve already finished (multi-launch)
+
+  if (tid == 0) {
+    for (int i = 0; i < A.nstage; ++i) {
+      mbar_init(&S.full[i], 33);   // producer lane-0 arrive (+tx) + 32 cp.async arrivals
+      mbar_init(&S.empty[i], NW);  // one arrival per consumer warp
+    }
+    S.done_pass = A.pass_begin - 1;
+    S.stop = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ======================================= producer =======================================
+  if (warp == NW) {
+    uint32_t stage = 0, phase = 0;
+    const uint64_t pol = policy_evict_first();
+    for (int p = A.pass_begin; p < A.pass_end; ++p) {
+      const int kind = pass_kind(p, A);
+      if (kind == PK_NONE) continue;
+      const int f = (kind == PK_V || kind == PK_ERR) ? 1 : 0;
+      const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
+      int wait_for = -1;
+      if (need_vold) wait_for = p - 2;                      // v_old written by pass p-2
+      if (A.tol_mode && kind == PK_U && p >= 4) wait_for = p - 1;   // stop decision
+      if (wait_for >= A.pass_begin) {
+        while (*(volatile int*)&S.done_pass < wait_for) __nanosleep(32);
+        __syncwarp();
+        __threadfence_block();
+        if (*(volatile int*)&S.stop) break;
+      }
+      int64_t r0, r1;
+      cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
+      const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
+      const float* vold = nullptr;
+      if (need_vold) vold = vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1);
+      const float* Fp = IMPL ? nullptr : A.F[f] + (int64_t)prob * A.fstride[f];
+      const float* Xp = IMPL ? A.X[f] + (int64_t)prob * A.fstride[f] : nullptr;
+      for (int64_t row0 = r0; row0 < r1; row0 += TR) {
+        const int rows = (int)min((int64_t)TR, r1 - row0);
+        mbar_wait(&S.empty[stage], phase ^ 1u);
+        float* st = ring + (int64_t)stage * A.stage_floats;
+        if (lane == 0) {
+          if constexpr (!IMPL) {
+            const uint32_t bytes = (uint32_t)rows * (uint32_t)r * 4u;
+            mbar_arrive_expect_tx(&S.full[stage], bytes);
+            bulk_g2s(st + kHdr, Fp + row0 * r, bytes, &S.full[stage], pol);
+          } else {
+            mbar_arrive(&S.full[stage]);
+          }
+        }
+        if (lane < rows) {
+          cp_async4(st + lane, wp + row0 + lane);
+          if (need_vold) cp_async4(st + 32 + lane, vold + row0 + lane);
+          if constexpr (IMPL) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) cp_async4(st + 64 + lane * 16 + c, Xp + (row0 + lane) * D + c);
+          }
+        }
+        cp_async_mbar_arrive_noinc(&S.full[stage]);
+        if (++stage == (uint32_t)A.nstage) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ======================================= consumers ======================================
+  const int R4 = r >> 2;
+  int g[NV];
+  bool gv[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    g[j] = tid + j * NT;
+    gv[j] = g[j] < R4;
+  }
+  float4 Wr[IMPL ? NV : 1][IMPL ? D : 1];
+  float4 b2[IMPL ? NV : 1];
+  if constexpr (IMPL) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if (gv[j]) {
+        b2[j] = *reinterpret_cast<const float4*>(A.beta2 + 4 * g[j]);
+#pragma unroll
+        for (int c = 0; c < D; ++c) Wr[j][c] = *reinterpret_cast<const float4*>(A.Wt + (int64_t)c * r + 4 * g[j]);
+      } else {
+        b2[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+        for (int c = 0; c < D; ++c) Wr[j][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+
+  float4 s[NV];
+  double acc64[NV][4];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+  }
+
+  // running read-out state (identical in every CTA of the problem)
+  double stA = __ldcg(stg_state + ST_A), stB = __ldcg(stg_state + ST_B);
+  double stBp = __ldcg(stg_state + ST_BPREV), stErr = __ldcg(stg_state + ST_ERR);
+  double stBrk = __ldcg(stg_state + ST_BRK);
+  const int64_t rstride = r + kExtra;
+  double* part = A.part + (int64_t)prob * rstride * A.gpp;
+  double* svec = A.svec + (int64_t)prob * rstride;
+  const bool multi = A.multi_launch != 0;
+
+  uint32_t stage = 0, phase = 0;
+  int buf = 0;
+  bool stopped = false;
+
+  for (int p = A.pass_begin;; ++p) {
+    // ---------------- results of pass q = p-1: read-out state and stopping test ------------
+    const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
+    if (have_prev) {
+      const int q = p - 1;
+      const int qk = pass_kind(q, A);
+      double e_err, e_slog, e_brk;
+      if (A.gpp > 1) {
+        e_err = __ldcg(svec + r);
+        e_slog = __ldcg(svec + r + 1);
+        e_brk = __ldcg(svec + r + 2);
+      } else {
+        e_err = S.ext[0];
+        e_slog = S.ext[1];
+        e_brk = S.ext[2];
+      }
+      stBrk += e_brk;
+      int final_t = -1;
+      double fA = 0.0, fB = 0.0, ferr = -1.0;
+      int conv = 0;
+      if (qk == PK_U) {
+        stA = e_slog;
+      } else if (qk == PK_V) {
+        stBp = stB;
+        stB = e_slog;
+        const int t = (q + 1) / 2;
+        if (t >= 2) {
+          stErr = e_err;   // err_{t-1} = |v^{t-1} o K^T u^{t-1} - b|_1
+          if (A.tol_mode && e_err < A.tol) {
+            final_t = t - 1; fA = stA; fB = stBp; ferr = e_err; conv = 1;
+          }
+        }
+      } else if (qk == PK_ERR) {
+        stErr = e_err;
+      }
+      if (final_t < 0 && q == A.num_passes - 1) {
+        final_t = A.T; fA = stA; fB = stB;
+        ferr = A.want_err ? stErr : -1.0;
+        conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
+      }
+      if (final_t >= 0) {
+        stopped = true;
+        if (tid == 0) S.stop = 1;
+        // the returned v lives in the workspace buffer: copy this CTA's rows to the user
+        if ((final_t ^ A.T) & 1) {
+          int64_t r0, r1;
+          cta_rows(A.rows[1], A.gpp, cta, &r0, &r1);
+          const float* src = A.vbuf1 + (int64_t)prob * A.wstride[1];
+          float* dst = A.out[1] + (int64_t)prob * A.wstride[1];
+          for (int64_t i = r0 + tid; i < r1; i += NT) dst[i] = src[i];
+        }
+        if (cta == 0 && tid == 0) {
+          stg_state[ST_ITERS] = (double)final_t;
+          stg_state[ST_ROT] = A.eps * (fA + fB);
+          stg_state[ST_FINAL_A] = fA;
+          stg_state[ST_FINAL_B] = fB;
+          stg_state[ST_ERR] = ferr;
+          stg_state[ST_CONV] = (double)conv;
+          stg_state[ST_BRK] = stBrk;
+          __threadfence();
+          stg_state[ST_STOP] = 1.0;
+        }
+      }
+      if (tid == 0) {
+        __threadfence_block();
+        *(volatile int*)&S.done_pass = q;
+      }
+      if (stopped) break;
+    }
+    if (p >= A.pass_end) break;
+
+    // ---------------- pass p ---------------------------------------------------------------
+    const int kind = pass_kind(p, A);
+    if (kind == PK_NONE) continue;
+    const int f = (kind == PK_V || kind == PK_ERR) ? 1 : 0;
+    if (kind != PK_INIT) {
+      if (A.gpp > 1) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (gv[j]) {
+            const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j]));
+            const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j] + 2));
+            s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+          } else {
+            s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+          s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+
+    int64_t r0, r1;
+    cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
+    float* outp = nullptr;
+    if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
+    if (kind == PK_V) outp = vbuf_ptr(A, prob, (p + 1) / 2);
+    const bool err_here = (kind == PK_ERR) || (kind == PK_V && p >= 3);
+    double errsum = 0.0, slogsum = 0.0, brksum = 0.0;
+    float4 acc32[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int tiles_since_flush = 0;
+
+    for (int64_t row0 = r0; row0 < r1; row0 += TR) {
+      const int rows = (int)min((int64_t)TR, r1 - row0);
+      mbar_wait(&S.full[stage], phase);
+      const float* st = ring + (int64_t)stage * A.stage_floats;
+      const float* feat = st + kHdr;
+
+      float fr[IMPL ? TR : 1][IMPL ? NV : 1][4];
+      if constexpr (IMPL) {
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          float x[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) x[c] = st[64 + i * 16 + c];
+          float al = 0.f;
+#pragma unroll
+          for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
+          al *= A.c2;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            float e0 = al + b2[j].x, e1 = al + b2[j].y, e2 = al + b2[j].z, e3 = al + b2[j].w;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              e0 = fmaf(Wr[j][c].x, x[c], e0);
+              e1 = fmaf(Wr[j][c].y, x[c], e1);
+              e2 = fmaf(Wr[j][c].z, x[c], e2);
+              e3 = fmaf(Wr[j][c].w, x[c], e3);
+            }
+            fr[i][j][0] = ex2(e0);
+            fr[i][j][1] = ex2(e1);
+            fr[i][j][2] = ex2(e2);
+            fr[i][j][3] = ex2(e3);
+          }
+        }
+      }
+
+      if (kind != PK_INIT) {
+        float pr[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          pr[i] = 0.f;
+          if (i < rows) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              if constexpr (IMPL) {
+                pr[i] = fmaf(fr[i][j][0], s[j].x, pr[i]);
+                pr[i] = fmaf(fr[i][j][1], s[j].y, pr[i]);
+                pr[i] = fmaf(fr[i][j][2], s[j].z, pr[i]);
+                pr[i] = fmaf(fr[i][j][3], s[j].w, pr[i]);
+              } else if (gv[j]) {
+                const float4 fv = lds128(feat + i * r + 4 * g[j]);
+                pr[i] = fmaf(fv.x, s[j].x, pr[i]);
+                pr[i] = fmaf(fv.y, s[j].y, pr[i]);
+                pr[i] = fmaf(fv.z, s[j].z, pr[i]);
+                pr[i] = fmaf(fv.w, s[j].w, pr[i]);
+              }
+            }
+          }
+        }
+        const float tot = warp_transpose_reduce<TR>(pr, lane);
+        constexpr int kLanesPerRow = 32 / TR;
+        if ((lane & (kLanesPerRow - 1)) == 0) S.red[buf][warp][lane / kLanesPerRow] = tot;
+        named_bar(1, NT);
+      }
+
+      if (tid < TR) {
+        float vr = 0.f;
+        if (tid < rows) {
+          if (kind == PK_INIT) {
+            vr = 1.f;   // u^0 = 1 (reading C6): s_v^0 = xi^T 1
+          } else {
+            float t = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) t += S.red[buf][w][tid];
+            const float c = st[tid];
+            if (err_here) errsum += fabs((double)st[32 + tid] * (double)t - (double)c);
+            if (kind != PK_ERR) {
+              vr = __fdiv_rn(c, t);
+              if (!(vr > 0.f) || !isfinite(vr)) brksum += 1.0;
+              outp[row0 + tid] = vr;
+              slogsum += (double)c * log((double)vr);
+            }
+          }
+        }
+        S.vrow[buf][tid] = vr;
+      }
+      named_bar(1, NT);
+
+      if (kind != PK_ERR) {
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          if (i < rows) {
+            const float vi = S.vrow[buf][i];
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              if constexpr (IMPL) {
+                acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
+                acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
+                acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
+                acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
+              } else if (gv[j]) {
+                const float4 fv = lds128(feat + i * r + 4 * g[j]);
+                acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
+                acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
+                acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
+                acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
+              }
+            }
+          }
+        }
+        if (++tiles_since_flush == kFlushTiles) {
+          tiles_since_flush = 0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            acc64[j][0] += (double)acc32[j].x;
+            acc64[j][1] += (double)acc32[j].y;
+            acc64[j][2] += (double)acc32[j].z;
+            acc64[j][3] += (double)acc32[j].w;
+            acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[stage]);
+      if (++stage == (uint32_t)A.nstage) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc64[j][0] += (double)acc32[j].x;
+      acc64[j][1] += (double)acc32[j].y;
+      acc64[j][2] += (double)acc32[j].z;
+      acc64[j][3] += (double)acc32[j].w;
+    }
+
+    // ---------------- end of pass: CTA extras, then cross-CTA fp64 reduction ----------------
+    if (tid < 32) {
+      S.xs[0][tid] = (tid < TR) ? errsum : 0.0;
+      S.xs[1][tid] = (tid < TR) ? slogsum : 0.0;
+      S.xs[2][tid] = (tid < TR) ? brksum : 0.0;
+    }
+    named_bar(1, NT);
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    if (tid == 0) {
+      for (int i = 0; i < TR; ++i) {
+        e0 += S.xs[0][i];
+        e1 += S.xs[1][i];
+        e2 += S.xs[2][i];
+      }
+    }
+    if (A.gpp > 1) {
+      // R1: column-major partials part[k * gpp + cta]
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (gv[j]) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) part[(int64_t)(4 * g[j] + q) * A.gpp + cta] = acc64[j][q];
+        }
+      }
+      if (tid == 0) {
+        part[(int64_t)(r + 0) * A.gpp + cta] = e0;
+        part[(int64_t)(r + 1) * A.gpp + cta] = e1;
+        part[(int64_t)(r + 2) * A.gpp + cta] = e2;
+        part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
+      }
+      group_barrier(A.bar + prob, (unsigned)(2 * p + 1) * (unsigned)A.gpp, tid);
+      // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
+      for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NW) {
+        const double* col = part + (int64_t)k * A.gpp;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
+        acc = warp_sum_f64(acc);
+        if (lane == 0) svec[k] = acc;
+      }
+      if (!multi) group_barrier(A.bar + prob, (unsigned)(2 * p + 2) * (unsigned)A.gpp, tid);
+    } else {
+      if (tid == 0) {
+        S.ext[0] = e0;
+        S.ext[1] = e1;
+        S.ext[2] = e2;
+      }
+      named_bar(1, NT);
+    }
+  }
+
+  // multi-launch mode: persist the running read-out state for the next launch
+  if (multi && !stopped && cta == 0 && tid == 0) {
+    stg_state[ST_A] = stA;
+    stg_state[ST_B] = stB;
+    stg_state[ST_BPREV] = stBp;
+    stg_state[ST_ERR] = stErr;
+    stg_state[ST_BRK] = stBrk;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv) {
+  const int r4 = (r + 3) / 4;
+  int v = (r4 + NT - 1) / NT;
+  int p2 = 1;
+  while (p2 < v) p2 <<= 1;
+  *nv = p2;
+  if (implicit) {
+    *tr = 8 / p2 > 0 ? 8 / p2 : 1;
+  } else if (p2 == 1) {
+    int t = 8192 / (r > 0 ? r : 1);
+    int tt = 32;
+    while (tt > t && tt > 8) tt >>= 1;
+    *tr = tt;
+  } else {
+    *tr = 8 / p2 > 0 ? 8 / p2 : 1;
+  }
+}
+
+size_t sinkhorn_static_smem() { return sizeof(Smem); }
+
+template <bool IMPL, int NV, int TR, int D>
+static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
+                            cudaStream_t s) {
+  auto kern = sinkhorn_kernel<IMPL, NV, TR, D>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  if (coop) {
+    void* args[] = {(void*)&a};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, s);
+  } else {
+    kern<<<grid, kThreads, smem, s>>>(a);
+    e = cudaGetLastError();
+  }
+  count_launch();
+  return e;
+}
+
+template <bool IMPL, int NV, int TR, int D>
+static int occupancy_t(size_t smem) {
+  int nb = 0;
+  auto kern = sinkhorn_kernel<IMPL, NV, TR, D>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
+  return nb;
+}
+
+#define LSK_STREAM_CASES(X) X(1, 32) X(1, 16) X(1, 8) X(2, 4) X(4, 2) X(8, 1)
+#define LSK_IMPL_D(X, NV, TR) X(NV, TR, 1) X(NV, TR, 2) X(NV, TR, 3) X(NV, TR, 4) \
+  X(NV, TR, 5) X(NV, TR, 6) X(NV, TR, 7) X(NV, TR, 8)
+
+cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool coop, int grid, size_t smem,
+                            cudaStream_t s) {
+  int tr, nv;
+  sinkhorn_tile_config(a.r, implicit, &tr, &nv);
+  if (!implicit) {
+#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return launch_t<false, NV_, TR_, 1>(a, coop, grid, smem, s);
+    LSK_STREAM_CASES(X)
+#undef X
+  } else {
+#define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && a.d == D_) return launch_t<true, NV_, TR_, D_>(a, coop, grid, smem, s);
+    LSK_IMPL_D(X, 1, 8) LSK_IMPL_D(X, 2, 4) LSK_IMPL_D(X, 4, 2)
+#undef X
+  }
+  return cudaErrorInvalidConfiguration;
+}
+
+int sinkhorn_max_ctas_per_sm(bool implicit, int r, int d, size_t smem) {
+  int tr, nv;
+  sinkhorn_tile_config(r, implicit, &tr, &nv);
+  if (!implicit) {
+#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return occupancy_t<false, NV_, TR_, 1>(smem);
+    LSK_STREAM_CASES(X)
+#undef X
+  } else {
+#define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && d == D_) return occupancy_t<true, NV_, TR_, D_>(smem);
+    LSK_IMPL_D(X, 1, 8) LSK_IMPL_D(X, 2, 4) LSK_IMPL_D(X, 4, 2)
+#undef X
+  }
+  return 0;
+}
+
+}  // namespace lsk

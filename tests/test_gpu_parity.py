@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Tolerances (north_star, BASELINE.json): ROT relative error <= 1e-5; u, v max
+relative error <= 1e-4 after the same iteration count; features <= 3e-5 relative (entries
+above 1e-30); integer work (Philox words) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ROT_TOL = 1e-5
+UV_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2006_07057_b200 as lib
+    return lib
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _maxrel(gpu, ref):
+    g = gpu.detach().cpu().double().numpy() if hasattr(gpu, "detach") else np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(g - ref) / np.abs(ref)))
+
+
+def _run_gpu(L, prob, T, variant="stream", tol=0.0, want_err=False, ctas_per_sm=0):
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    return L.rot(X, Y, a, b, prob["eps"], prob["r"], prob["seed"], iters=T, tol=tol,
+                 variant=variant, want_err=want_err, ctas_per_sm=ctas_per_sm)
+
+
+def _check_parity(res, ref, rot_tol=ROT_TOL, uv_tol=UV_TOL):
+    rot_err = abs(res["rot"] - ref["rot"]) / abs(ref["rot"])
+    u_err = _maxrel(res["u"], ref["u"])
+    v_err = _maxrel(res["v"], ref["v"])
+    assert rot_err <= rot_tol and u_err <= uv_tol and v_err <= uv_tol, (rot_err, u_err, v_err)
+    return rot_err, u_err, v_err
+
+
+# ------------------------------------------------------------------ a2: generator --------
+def test_philox_words_bit_exact(L):
+    import torch
+    for seed, r, d in [(7058, 100, 2), (2 ** 40 + 17, 333, 5), (0, 4096, 3), (7061, 512, 128)]:
+        out = torch.zeros((r, (d + 3) // 4, 4), dtype=torch.int32, device="cuda")
+        L.lsk_philox_words(seed, r, d, out)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, O.philox_words(r, d, seed))
+
+
+@pytest.mark.parametrize("cfg_key", [1, 2, 3, 4, 5])
+def test_anchors_match_oracle(L, cfg_key):
+    import torch
+    cfg = synth.get_config(cfg_key)
+    R = 1.0 + 0.1 * cfg_key
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, cfg.r, R, cfg.anchor_seed)
+    U = torch.empty((cfg.r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    ref = O.draw_anchors(cfg.r, cfg.d, O.gaussian_params(cfg.eps, cfg.d, cfg.r, R)["sigma"],
+                         cfg.anchor_seed).astype(np.float32)
+    got = U.cpu().numpy()
+    ulps = np.abs(got.view(np.int32).astype(np.int64) - ref.view(np.int32).astype(np.int64))
+    assert ulps.max() <= 1, ulps.max()
+    assert (ulps == 0).mean() > 0.999
+
+
+# ------------------------------------------------------------------ a1 auto R ------------
+def test_auto_R_matches_oracle(L):
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=5000, m=4000)
+    p = L.lsk_feature_params_init(cfg.eps, 2, cfg.r, 0.0, 1, _dev(prob["X"]), _dev(prob["Y"]))
+    assert abs(p.R - O.max_norm(prob["X"], prob["Y"])) <= 1e-15 * p.R
+    with pytest.raises(L.LskError) as e:
+        L.lsk_feature_params_init(cfg.eps, 2, cfg.r, 0.5 * p.R, 1, _dev(prob["X"]), _dev(prob["Y"]))
+    assert e.value.status == -3
+
+
+# ------------------------------------------------------------------ a3: feature map ------
+@pytest.mark.parametrize("cfg_key,n", [(1, 500), (2, 3001), (3, 1001), (4, 777), (5, 2049)])
+def test_feature_map_matches_oracle(L, cfg_key, n):
+    import torch
+    cfg = synth.get_config(cfg_key)
+    prob = synth.make_problem(cfg, n=n, m=n)
+    R = O.max_norm(prob["X"], prob["Y"])
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, cfg.r, R, cfg.anchor_seed)
+    U = torch.empty((cfg.r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((n, cfg.r), dtype=torch.float32, device="cuda")
+    L.lsk_feature_map(p, U, _dev(prob["X"]), Xi)
+    torch.cuda.synchronize()
+    Uo = U.cpu().double().numpy()          # anchor parity is tested separately (<= 1 ulp)
+    ref = O.feature_matrix(prob["X"], Uo, cfg.eps, p.q).T
+    got = Xi.cpu().double().numpy()
+    mask = ref > 1e-30
+    rel = np.abs(got[mask] - ref[mask]) / ref[mask]
+    tol = 3e-5 if cfg.d <= 16 else 1e-4
+    assert rel.max() <= tol, rel.max()
+    assert np.all(got[~mask] < 1e-29)
+    assert np.all(got >= 0)
+
+
+# ------------------------------------------------------------------ Sinkhorn parity ------
+def test_config1_full_streaming(L):
+    cfg = synth.get_config(1)
+    prob = synth.make_problem(cfg)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=cfg.T)
+    res = _run_gpu(L, prob, cfg.T)
+    _check_parity(res, ref)
+    assert res["report"]["iters"] == cfg.T
+
+
+def test_config1_full_implicit(L):
+    cfg = synth.get_config(1)
+    prob = synth.make_problem(cfg)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=cfg.T)
+    res = _run_gpu(L, prob, cfg.T, variant="implicit")
+    _check_parity(res, ref)
+
+
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
+def test_config2_reduced_ragged(L, variant):
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=4099, m=3907)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=cfg.T)
+    res = _run_gpu(L, prob, cfg.T, variant=variant)
+    _check_parity(res, ref)
+
+
+def test_config3_reduced_dirichlet(L):
+    cfg = synth.get_config(3)
+    prob = synth.make_problem(cfg, n=3001, m=2999)
+    T = 300
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
+    res = _run_gpu(L, prob, T)
+    _check_parity(res, ref)
+
+
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
+def test_config5_reduced(L, variant):
+    cfg = synth.get_config(5)
+    prob = synth.make_problem(cfg, n=6151, m=6143)
+    T = 60
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
+    res = _run_gpu(L, prob, T, variant=variant)
+    _check_parity(res, ref)
+
+
+def test_config4_batched_matches_oracle_and_single(L):
+    import torch
+    cfg = synth.get_config(4)
+    B, T = 3, cfg.T
+    bp = synth.make_batched(cfg, batch=B, n=1031, m=1029)
+    X, Y, a, b = (_dev(bp[k]) for k in ("X", "Y", "a", "b"))
+    R = O.max_norm(bp["X"].reshape(-1, cfg.d), bp["Y"].reshape(-1, cfg.d))
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, cfg.r, R, cfg.anchor_seed)
+    U = torch.empty((cfg.r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((B, 1031, cfg.r), dtype=torch.float32, device="cuda")
+    Ze = torch.empty((B, 1029, cfg.r), dtype=torch.float32, device="cuda")
+    L.lsk_feature_map_batched(p, U, X, Xi)
+    L.lsk_feature_map_batched(p, U, Y, Ze)
+    u = torch.empty((B, 1031), device="cuda")
+    v = torch.empty((B, 1029), device="cuda")
+    reps = L.lsk_factored_sinkhorn_batched(Xi, Ze, a, b, cfg.eps, L.make_opts(T), u, v)
+    rots = L.lsk_rot_value_batched(u, v, a, b, cfg.eps)
+    for k in range(B):
+        ref = O.rot(bp["X"][k], bp["Y"][k], bp["a"][k], bp["b"][k], cfg.eps, cfg.r,
+                    cfg.anchor_seed, T=T, R=R)
+        _check_parity(dict(rot=reps[k].rot, u=u[k], v=v[k]), ref)
+        assert abs(rots[k] - reps[k].rot) <= 1e-12 * abs(reps[k].rot)
+        # batched == single solve of the same pair (same kernels, bit-identical)
+        u1 = torch.empty(1031, device="cuda")
+        v1 = torch.empty(1029, device="cuda")
+        rep1 = L.lsk_factored_sinkhorn(Xi[k], Ze[k], a[k], b[k], cfg.eps, L.make_opts(T), u1, v1)
+        assert abs(rep1.rot - reps[k].rot) <= 1e-6 * abs(rep1.rot)
+        assert _maxrel(u1, u[k].cpu().double().numpy()) <= 1e-5
+
+
+# ------------------------------------------------------------------ modes & properties ----
+def test_tolerance_mode(L):
+    cfg = synth.get_config(1)
+    prob = synth.make_problem(cfg)
+    tol = 1e-5
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, tol=tol)
+    for variant in ("stream", "implicit"):
+        res = _run_gpu(L, prob, 500, variant=variant, tol=tol)
+        rep = res["report"]
+        assert rep["converged"] == 1 and rep["marginal_err"] < tol
+        assert abs(rep["iters"] - ref["iters"]) <= 1, (rep["iters"], ref["iters"])
+        if rep["iters"] == ref["iters"]:
+            _check_parity(res, ref)
+
+
+def test_fixed_T_marginal_error(L):
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=2000, m=2000)
+    T = 7
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T,
+                record_err=True)
+    res = _run_gpu(L, prob, T, want_err=True)
+    err = res["report"]["marginal_err"]
+    assert abs(err - ref["errs"][-1]) <= 1e-3 * ref["errs"][-1] + 1e-7, (err, ref["errs"][-1])
+
+
+def test_deterministic(L):
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=20000, m=20000)
+    r1 = _run_gpu(L, prob, 50)
+    r2 = _run_gpu(L, prob, 50)
+    assert r1["rot"] == r2["rot"]
+    assert bool((r1["u"] == r2["u"]).all()) and bool((r1["v"] == r2["v"]).all())
+
+
+def test_single_point_and_tiny(L):
+    """n = m = 1: W_hat = c_theta(x, y) (P9); r = 4 minimal; more CTAs than rows."""
+    rng = np.random.default_rng(5)
+    x = (rng.normal(size=(1, 3)) * 0.3).astype(np.float32)
+    y = (rng.normal(size=(1, 3)) * 0.3).astype(np.float32)
+    one = np.ones(1, np.float32)
+    for r in (4, 64):
+        prob = dict(X=x, Y=y, a=one, b=one, eps=0.7, r=r, seed=5)
+        res = _run_gpu(L, prob, 3)
+        ref = O.rot(x, y, one, one, 0.7, r, 5, T=3)
+        kappa = float(ref["xi"][:, 0] @ ref["zeta"][:, 0])
+        assert abs(res["rot"] - (-0.7 * math.log(kappa))) <= 1e-5 * abs(res["rot"]) + 1e-6
+    prob = synth.random_small(3, 37, 5, 2)
+    prob.update(eps=0.5, r=8, seed=1)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], 0.5, 8, 1, T=40)
+    for variant in ("stream", "implicit"):
+        _check_parity(_run_gpu(L, prob, 40, variant=variant), ref)
+
+
+def test_rank_one_full_size_closed_form(L):
+    """Config 5 at FULL size with identical points: K_theta = kappa 11^T, so one loop gives
+    W = eps(sum a ln a + sum b ln b - (sum b) ln kappa + (sum a - sum b) ln n
+    - (sum a) ln sum b) (P11).  Exercises every row of the full launch configuration."""
+    cfg = synth.get_config(5)
+    prob = synth.make_problem(cfg, identical_points=True)
+    res = _run_gpu(L, prob, 2, variant="implicit")
+    U = res["U"].cpu().double().numpy()
+    q = res["params"]["q"]
+    xi0 = O.feature_entries_scaled(prob["X"][:1], U, cfg.eps, q, cfg.r, np.zeros(cfg.r, int), np.arange(cfg.r))
+    ze0 = O.feature_entries_scaled(prob["Y"][:1], U, cfg.eps, q, cfg.r, np.zeros(cfg.r, int), np.arange(cfg.r))
+    kappa = float(xi0 @ ze0)
+    a, b = prob["a"].astype(np.float64), prob["b"].astype(np.float64)
+    n = len(a)
+    expect = cfg.eps * (a @ np.log(a) + b @ np.log(b) - b.sum() * math.log(kappa)
+                        + (a.sum() - b.sum()) * math.log(n) - a.sum() * math.log(b.sum()))
+    assert abs(res["rot"] - expect) <= 1e-5 * abs(expect), (res["rot"], expect)
+
+
+def test_rot_value_matches_oracle(L):
+    rng = np.random.default_rng(11)
+    n, m = 100003, 77777
+    u = rng.uniform(0.1, 10, n).astype(np.float32)
+    v = rng.uniform(0.1, 10, m).astype(np.float32)
+    a = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    b = rng.uniform(0.5, 1.5, m).astype(np.float32)
+    got = L.lsk_rot_value(_dev(u), _dev(v), _dev(a), _dev(b), 0.3)
+    ref = O.dual_estimate(u.astype(np.float64), v.astype(np.float64), a, b, 0.3)
+    assert abs(got - ref) <= 1e-12 * abs(ref)
+
+
+def test_host_entry_point_matches_device_path(L):
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=3000, m=3000)
+    dev = _run_gpu(L, prob, 100)
+    u = np.empty(3000, np.float32)
+    v = np.empty(3000, np.float32)
+    rep = L.lsk_rot_host(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r,
+                         cfg.anchor_seed, L.make_opts(100), variant=1, u_out=u, v_out=v)
+    assert rep.rot == dev["rot"]
+    assert np.array_equal(u, dev["u"].cpu().numpy())
+
+
+@pytest.mark.slow
+def test_config2_full_size(L):
+    """Config 2 at its full size (n=m=40000, r=1000, T=500) in the bench's launch config."""
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=cfg.T)
+    for variant in ("stream", "implicit"):
+        _check_parity(_run_gpu(L, prob, cfg.T, variant=variant), ref)
