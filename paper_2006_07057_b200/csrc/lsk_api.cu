@@ -198,12 +198,14 @@ static lsk_status plan_solve(const SinkArgs& A, bool impl, int batch, const lsk_
   const size_t stage_bytes = (size_t)sf * 4;
   int nst = (int)((per_cta - static_smem - 512) / stage_bytes);
   nst = std::min(nst, impl ? 8 : 16);
-  if (nst < 2) {
+  if (nst < 3) {
     cps = 1;
     nst = (int)((std::min<size_t>(max_smem_optin(), smem_sm) - static_smem - 512) / stage_bytes);
     nst = std::min(nst, 16);
-    if (nst < 2) return fail(LSK_EDIM, "r too large: two ring stages do not fit in shared memory");
+    if (nst < 3) return fail(LSK_EDIM, "r too large: three ring stages do not fit in shared memory");
   }
+  // the pipelined tile loop holds two stages while the producer fills a third
+  if (const char* e = getenv("LSK_NSTAGE")) nst = std::max(3, std::min(nst, atoi(e)));   // tuning knob
   c->nstage = nst;
   c->smem = (size_t)nst * stage_bytes;
   int occ = sinkhorn_max_ctas_per_sm(impl, A.r, A.d, c->smem);
@@ -218,6 +220,7 @@ static lsk_status plan_solve(const SinkArgs& A, bool impl, int batch, const lsk_
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
     const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
     c->gpp = (int)std::min<int64_t>((int64_t)sms * cps, want);
+    if (const char* e = getenv("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
     c->coop = c->gpp > 1;
   }
@@ -243,6 +246,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     c.coop = true;
   }
   A.gpp = c.gpp;
+  A.dbg = getenv("LSK_DEBUG") ? atoi(getenv("LSK_DEBUG")) : 0;
   A.nprob = batch;
   A.nstage = c.nstage;
   A.stage_floats = c.stage_floats;
@@ -273,6 +277,10 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
                                             ncclSum, comm->comm, s),
                            "ncclAllReduce"));
     }
+    // read-out partials a^T log u, b^T log v of the local rows -> global sums
+    LSK_TRY(nccl_check(nccl().allReduce(A.state + ST_FINAL_A, A.state + ST_FINAL_A, 2,
+                                        ncclFloat64, ncclSum, comm->comm, s),
+                       "ncclAllReduce(read-out)"));
   }
   if (reps) {
     std::vector<double> st((size_t)kStateDoubles * batch);
@@ -285,7 +293,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       rp.iters = (int32_t)x[ST_ITERS];
       rp.converged = (int32_t)x[ST_CONV];
       rp.marginal_err = x[ST_ERR];
-      rp.rot = x[ST_ROT];
+      rp.rot = comm ? A.eps * (x[ST_FINAL_A] + x[ST_FINAL_B]) : x[ST_ROT];
       rp.sum_a_log_u = x[ST_FINAL_A];
       rp.sum_b_log_v = x[ST_FINAL_B];
       rp.breakdown = x[ST_BRK] > 0 ? 1 : 0;

@@ -10,13 +10,10 @@ namespace lsk {
 constexpr int kConsumerThreads = 256;              // 8 consumer warps per CTA
 constexpr int kThreads = kConsumerThreads + 32;    // + 1 producer warp
 constexpr int kExtra = 4;                          // extras appended to every r-vector:
-                                                   // [0]=err, [1]=slog, [2]=breakdown, [3]=0
+                                                   // [0]=err, [1]=breakdown, [2..3]=0
 constexpr int kStateDoubles = 16;                  // per-problem solve state block
 // state block layout (doubles)
 enum StateIdx {
-  ST_A = 0,        // a^T log u of the latest u-pass
-  ST_B = 1,        // b^T log v of the latest v-pass
-  ST_BPREV = 2,    // b^T log v of the v-pass before it
   ST_ERR = 3,      // latest marginal error
   ST_STOP = 4,     // 1 once the solve has finished (early stop or last pass)
   ST_ITERS = 5,    // iterations of the returned state
@@ -64,6 +61,7 @@ struct SinkArgs {
   const float* Wt;         // [d][r]  W_kc = (4 log2e / eps) U_kc, transposed
   const float* beta2;      // [r]     log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
   float c2;                // -2 log2e / eps
+  int dbg;                 // tuning only: 1 = consumers release stages without computing
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.

@@ -40,9 +40,9 @@ constexpr int kMaxStages = 16;
 struct Smem {
   uint64_t full[kMaxStages];
   uint64_t empty[kMaxStages];
-  float red[2][NW][32];
-  float vrow[2][32];
-  double xs[3][32];
+  uint64_t redbar[3];
+  float red[3][NW][32];
+  double xs[2][NW];
   double ext[kExtra];
   int done_pass;
   int stop;
@@ -125,10 +125,15 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       mbar_init(&S.full[i], 33);   // producer lane-0 arrive (+tx) + 32 cp.async arrivals
       mbar_init(&S.empty[i], NW);  // one arrival per consumer warp
     }
+    for (int i = 0; i < 3; ++i) mbar_init(&S.redbar[i], NT);
     S.done_pass = A.pass_begin - 1;
     S.stop = 0;
     fence_mbar_init();
   }
+  // zero the ring once: tail tiles then compute on finite data without per-row predicates
+  for (int64_t i = tid; i < (int64_t)A.nstage * A.stage_floats / 4; i += kThreads)
+    reinterpret_cast<float4*>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  fence_proxy_async_smem();
   __syncthreads();
 
   // ======================================= producer =======================================
@@ -192,9 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   int g[NV];
   bool gv[NV];
 #pragma unroll
+  int ge[NV];   // clamped group index: invalid groups read column group 0 and use s = 0
+#pragma unroll
   for (int j = 0; j < NV; ++j) {
     g[j] = tid + j * NT;
     gv[j] = g[j] < R4;
+    ge[j] = gv[j] ? g[j] : 0;
   }
   float4 Wr[IMPL ? NV : 1][IMPL ? D : 1];
   float4 b2[IMPL ? NV : 1];
@@ -222,87 +230,59 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
   }
 
-  // running read-out state (identical in every CTA of the problem)
-  double stA = __ldcg(stg_state + ST_A), stB = __ldcg(stg_state + ST_B);
-  double stBp = __ldcg(stg_state + ST_BPREV), stErr = __ldcg(stg_state + ST_ERR);
+  // running solve state (identical in every CTA of the problem)
+  double stErr = __ldcg(stg_state + ST_ERR);
   double stBrk = __ldcg(stg_state + ST_BRK);
   const int64_t rstride = r + kExtra;
   double* part = A.part + (int64_t)prob * rstride * A.gpp;
   double* svec = A.svec + (int64_t)prob * rstride;
   const bool multi = A.multi_launch != 0;
+  unsigned int nbar = 0;   // group barriers passed in this launch (counter zeroed per launch)
 
   uint32_t stage = 0, phase = 0;
-  int buf = 0;
-  bool stopped = false;
+  uint32_t tk = 0;         // tiles that used a red buffer (buffer tk % 3, phase (tk / 3) & 1)
+  int final_t = -1, conv = 0;
+  double ferr = -1.0;
 
   for (int p = A.pass_begin;; ++p) {
-    // ---------------- results of pass q = p-1: read-out state and stopping test ------------
+    // ---------------- results of pass q = p-1: stopping test ----------------------------------
     const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
     if (have_prev) {
       const int q = p - 1;
       const int qk = pass_kind(q, A);
-      double e_err, e_slog, e_brk;
+      double e_err, e_brk;
       if (A.gpp > 1) {
         e_err = __ldcg(svec + r);
-        e_slog = __ldcg(svec + r + 1);
-        e_brk = __ldcg(svec + r + 2);
+        e_brk = __ldcg(svec + r + 1);
       } else {
         e_err = S.ext[0];
-        e_slog = S.ext[1];
-        e_brk = S.ext[2];
+        e_brk = S.ext[1];
       }
       stBrk += e_brk;
-      int final_t = -1;
-      double fA = 0.0, fB = 0.0, ferr = -1.0;
-      int conv = 0;
-      if (qk == PK_U) {
-        stA = e_slog;
-      } else if (qk == PK_V) {
-        stBp = stB;
-        stB = e_slog;
+      if (qk == PK_V) {
         const int t = (q + 1) / 2;
         if (t >= 2) {
-          stErr = e_err;   // err_{t-1} = |v^{t-1} o K^T u^{t-1} - b|_1
+          stErr = e_err;   // err_{t-1} = |v^{t-1} o K^T u^{t-1} - b|_1  (PAPER.md:239)
           if (A.tol_mode && e_err < A.tol) {
-            final_t = t - 1; fA = stA; fB = stBp; ferr = e_err; conv = 1;
+            final_t = t - 1;
+            ferr = e_err;
+            conv = 1;
           }
         }
       } else if (qk == PK_ERR) {
         stErr = e_err;
       }
       if (final_t < 0 && q == A.num_passes - 1) {
-        final_t = A.T; fA = stA; fB = stB;
+        final_t = A.T;
         ferr = A.want_err ? stErr : -1.0;
         conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
       }
-      if (final_t >= 0) {
-        stopped = true;
-        if (tid == 0) S.stop = 1;
-        // the returned v lives in the workspace buffer: copy this CTA's rows to the user
-        if ((final_t ^ A.T) & 1) {
-          int64_t r0, r1;
-          cta_rows(A.rows[1], A.gpp, cta, &r0, &r1);
-          const float* src = A.vbuf1 + (int64_t)prob * A.wstride[1];
-          float* dst = A.out[1] + (int64_t)prob * A.wstride[1];
-          for (int64_t i = r0 + tid; i < r1; i += NT) dst[i] = src[i];
-        }
-        if (cta == 0 && tid == 0) {
-          stg_state[ST_ITERS] = (double)final_t;
-          stg_state[ST_ROT] = A.eps * (fA + fB);
-          stg_state[ST_FINAL_A] = fA;
-          stg_state[ST_FINAL_B] = fB;
-          stg_state[ST_ERR] = ferr;
-          stg_state[ST_CONV] = (double)conv;
-          stg_state[ST_BRK] = stBrk;
-          __threadfence();
-          stg_state[ST_STOP] = 1.0;
-        }
-      }
       if (tid == 0) {
+        if (final_t >= 0) S.stop = 1;
         __threadfence_block();
         *(volatile int*)&S.done_pass = q;
       }
-      if (stopped) break;
+      if (final_t >= 0) break;
     }
     if (p >= A.pass_end) break;
 
@@ -325,7 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       } else {
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-          s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
+          s[j] = gv[j] ? make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2],
+                                     (float)acc64[j][3])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
 #pragma unroll
@@ -339,19 +321,111 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
     if (kind == PK_V) outp = vbuf_ptr(A, prob, (p + 1) / 2);
     const bool err_here = (kind == PK_ERR) || (kind == PK_V && p >= 3);
-    double errsum = 0.0, slogsum = 0.0, brksum = 0.0;
+    double errsum = 0.0, brksum = 0.0;   // warp 0, lanes < TR
     float4 acc32[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     int tiles_since_flush = 0;
 
-    for (int64_t row0 = r0; row0 < r1; row0 += TR) {
+    // Software-pipelined tile loop: tile k's row dots are reduced across warps through
+    // red[k % 3] + an mbarrier (split arrive / wait), and finished (scaling, accumulation,
+    // stage release) only after tile k+1's dots are issued — no CTA-wide barrier per tile.
+    float frA[IMPL ? TR : 1][IMPL ? NV : 1][4];
+    float frB[IMPL ? TR : 1][IMPL ? NV : 1][4];
+    int64_t row0 = r0;
+    bool pend = false;              // a tile whose dots are issued but not finished
+    bool pend_in_A = false;
+    int64_t p_row0 = 0;
+    int p_rows = 0;
+    uint32_t p_stage = 0, p_tk = 0;
+
+    // finish a tile: wait for all warps' partial dots, derive the TR scalings (every warp
+    // computes them identically), write them (warp 0), accumulate F_j^T w_j, release the stage
+    auto finish = [&](float (&fr)[IMPL ? TR : 1][IMPL ? NV : 1][4], uint32_t fstage,
+                      int64_t frow0, int frows, uint32_t ftk) {
+      const float* st = ring + (int64_t)fstage * A.stage_floats;
+      const float* feat = st + kHdr;
+      float vr_l = 0.f;
+      if (kind == PK_INIT) {
+        vr_l = (lane < frows) ? 1.f : 0.f;   // u^0 = 1 (reading C6): s_v^0 = xi^T 1
+      } else {
+        const int rb = (int)(ftk % 3u);
+        mbar_wait(&S.redbar[rb], (ftk / 3u) & 1u);
+        if (lane < frows) {
+          float t = 0.f;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) t += S.red[rb][w][lane];   // fixed order: all warps agree
+          const float c = st[lane];
+          if (kind != PK_ERR) vr_l = __fdiv_rn(c, t);
+          if (warp == 0) {
+            if (err_here) errsum += fabs((double)st[32 + lane] * (double)t - (double)c);
+            if (kind != PK_ERR) {
+              if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
+              outp[frow0 + lane] = vr_l;
+            }
+          }
+        }
+      }
+      if (kind != PK_ERR) {
+        // vr_l = 0 in lanes >= frows, so tail rows add 0 x (finite stale/zero data)
+        float4 fvv[IMPL ? 1 : TR][IMPL ? 1 : NV];
+        if constexpr (!IMPL) {
+#pragma unroll
+          for (int i = 0; i < TR; ++i)
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+              fvv[i][j] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            if constexpr (IMPL) {
+              acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
+              acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
+              acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
+              acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
+            } else {
+              const float4 fv = fvv[i][j];
+              acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
+              acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
+              acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
+              acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
+            }
+          }
+        }
+        if (++tiles_since_flush == kFlushTiles) {
+          tiles_since_flush = 0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            acc64[j][0] += (double)acc32[j].x;
+            acc64[j][1] += (double)acc32[j].y;
+            acc64[j][2] += (double)acc32[j].z;
+            acc64[j][3] += (double)acc32[j].w;
+            acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[fstage]);
+    };
+
+    // issue tile at row0 into `cur`; then finish the pending tile (held in `prv`)
+    auto step = [&](float (&cur)[IMPL ? TR : 1][IMPL ? NV : 1][4],
+                    float (&prv)[IMPL ? TR : 1][IMPL ? NV : 1][4], bool cur_is_A) -> bool {
+      if (row0 >= r1) return false;
       const int rows = (int)min((int64_t)TR, r1 - row0);
       mbar_wait(&S.full[stage], phase);
+      if (A.dbg == 1) {   // tuning probe: pure streaming rate of the producer / TMA ring
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[stage]);
+        if (++stage == (uint32_t)A.nstage) { stage = 0; phase ^= 1u; }
+        row0 += TR;
+        return true;
+      }
       const float* st = ring + (int64_t)stage * A.stage_floats;
       const float* feat = st + kHdr;
-
-      float fr[IMPL ? TR : 1][IMPL ? NV : 1][4];
       if constexpr (IMPL) {
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
@@ -372,107 +446,70 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
               e2 = fmaf(Wr[j][c].z, x[c], e2);
               e3 = fmaf(Wr[j][c].w, x[c], e3);
             }
-            fr[i][j][0] = ex2(e0);
-            fr[i][j][1] = ex2(e1);
-            fr[i][j][2] = ex2(e2);
-            fr[i][j][3] = ex2(e3);
+            cur[i][j][0] = ex2(e0);
+            cur[i][j][1] = ex2(e1);
+            cur[i][j][2] = ex2(e2);
+            cur[i][j][3] = ex2(e3);
           }
         }
       }
-
+      uint32_t my_tk = tk;
       if (kind != PK_INIT) {
+        // rows >= `rows` of a tail tile hold finite stale/zero data; their dots are unused
         float pr[TR];
+        float4 fvv[IMPL ? 1 : TR][IMPL ? 1 : NV];
+        if constexpr (!IMPL) {
+#pragma unroll
+          for (int i = 0; i < TR; ++i)
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+              fvv[i][j] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+        }
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
           pr[i] = 0.f;
-          if (i < rows) {
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-              if constexpr (IMPL) {
-                pr[i] = fmaf(fr[i][j][0], s[j].x, pr[i]);
-                pr[i] = fmaf(fr[i][j][1], s[j].y, pr[i]);
-                pr[i] = fmaf(fr[i][j][2], s[j].z, pr[i]);
-                pr[i] = fmaf(fr[i][j][3], s[j].w, pr[i]);
-              } else if (gv[j]) {
-                const float4 fv = lds128(feat + i * r + 4 * g[j]);
-                pr[i] = fmaf(fv.x, s[j].x, pr[i]);
-                pr[i] = fmaf(fv.y, s[j].y, pr[i]);
-                pr[i] = fmaf(fv.z, s[j].z, pr[i]);
-                pr[i] = fmaf(fv.w, s[j].w, pr[i]);
-              }
+          for (int j = 0; j < NV; ++j) {
+            if constexpr (IMPL) {
+              pr[i] = fmaf(cur[i][j][0], s[j].x, pr[i]);
+              pr[i] = fmaf(cur[i][j][1], s[j].y, pr[i]);
+              pr[i] = fmaf(cur[i][j][2], s[j].z, pr[i]);
+              pr[i] = fmaf(cur[i][j][3], s[j].w, pr[i]);
+            } else {
+              const float4 fv = fvv[i][j];
+              pr[i] = fmaf(fv.x, s[j].x, pr[i]);
+              pr[i] = fmaf(fv.y, s[j].y, pr[i]);
+              pr[i] = fmaf(fv.z, s[j].z, pr[i]);
+              pr[i] = fmaf(fv.w, s[j].w, pr[i]);
             }
           }
         }
         const float tot = warp_transpose_reduce<TR>(pr, lane);
         constexpr int kLanesPerRow = 32 / TR;
-        if ((lane & (kLanesPerRow - 1)) == 0) S.red[buf][warp][lane / kLanesPerRow] = tot;
-        named_bar(1, NT);
+        const int rb = (int)(tk % 3u);
+        if ((lane & (kLanesPerRow - 1)) == 0) S.red[rb][warp][lane / kLanesPerRow] = tot;
+        mbar_arrive(&S.redbar[rb]);   // every consumer lane arrives (count NT)
+        ++tk;
       }
-
-      if (tid < TR) {
-        float vr = 0.f;
-        if (tid < rows) {
-          if (kind == PK_INIT) {
-            vr = 1.f;   // u^0 = 1 (reading C6): s_v^0 = xi^T 1
-          } else {
-            float t = 0.f;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) t += S.red[buf][w][tid];
-            const float c = st[tid];
-            if (err_here) errsum += fabs((double)st[32 + tid] * (double)t - (double)c);
-            if (kind != PK_ERR) {
-              vr = __fdiv_rn(c, t);
-              if (!(vr > 0.f) || !isfinite(vr)) brksum += 1.0;
-              outp[row0 + tid] = vr;
-              slogsum += (double)c * log((double)vr);
-            }
-          }
-        }
-        S.vrow[buf][tid] = vr;
-      }
-      named_bar(1, NT);
-
-      if (kind != PK_ERR) {
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          if (i < rows) {
-            const float vi = S.vrow[buf][i];
-#pragma unroll
-            for (int j = 0; j < NV; ++j) {
-              if constexpr (IMPL) {
-                acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
-                acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
-                acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
-                acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
-              } else if (gv[j]) {
-                const float4 fv = lds128(feat + i * r + 4 * g[j]);
-                acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
-                acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
-                acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
-                acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
-              }
-            }
-          }
-        }
-        if (++tiles_since_flush == kFlushTiles) {
-          tiles_since_flush = 0;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            acc64[j][0] += (double)acc32[j].x;
-            acc64[j][1] += (double)acc32[j].y;
-            acc64[j][2] += (double)acc32[j].z;
-            acc64[j][3] += (double)acc32[j].w;
-            acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[stage]);
+      if (pend) finish(prv, p_stage, p_row0, p_rows, p_tk);
+      pend = true;
+      pend_in_A = cur_is_A;
+      p_stage = stage;
+      p_row0 = row0;
+      p_rows = rows;
+      p_tk = my_tk;
       if (++stage == (uint32_t)A.nstage) {
         stage = 0;
         phase ^= 1u;
       }
-      buf ^= 1;
+      row0 += TR;
+      return true;
+    };
+    while (step(frA, frB, true) && step(frB, frA, false)) {
+    }
+    if (pend) {
+      if (pend_in_A) finish(frA, p_stage, p_row0, p_rows, p_tk);
+      else finish(frB, p_stage, p_row0, p_rows, p_tk);
     }
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -483,19 +520,10 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     }
 
     // ---------------- end of pass: CTA extras, then cross-CTA fp64 reduction ----------------
-    if (tid < 32) {
-      S.xs[0][tid] = (tid < TR) ? errsum : 0.0;
-      S.xs[1][tid] = (tid < TR) ? slogsum : 0.0;
-      S.xs[2][tid] = (tid < TR) ? brksum : 0.0;
-    }
-    named_bar(1, NT);
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-    if (tid == 0) {
-      for (int i = 0; i < TR; ++i) {
-        e0 += S.xs[0][i];
-        e1 += S.xs[1][i];
-        e2 += S.xs[2][i];
-      }
+    double e0 = 0.0, e1 = 0.0;
+    if (warp == 0) {
+      e0 = warp_sum_f64(errsum);
+      e1 = warp_sum_f64(brksum);
     }
     if (A.gpp > 1) {
       // R1: column-major partials part[k * gpp + cta]
@@ -509,10 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (tid == 0) {
         part[(int64_t)(r + 0) * A.gpp + cta] = e0;
         part[(int64_t)(r + 1) * A.gpp + cta] = e1;
-        part[(int64_t)(r + 2) * A.gpp + cta] = e2;
+        part[(int64_t)(r + 2) * A.gpp + cta] = 0.0;
         part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
       }
-      group_barrier(A.bar + prob, (unsigned)(2 * p + 1) * (unsigned)A.gpp, tid);
+      group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
       for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NW) {
         const double* col = part + (int64_t)k * A.gpp;
@@ -522,22 +550,77 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         acc = warp_sum_f64(acc);
         if (lane == 0) svec[k] = acc;
       }
-      if (!multi) group_barrier(A.bar + prob, (unsigned)(2 * p + 2) * (unsigned)A.gpp, tid);
+      if (!multi) group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
     } else {
       if (tid == 0) {
         S.ext[0] = e0;
         S.ext[1] = e1;
-        S.ext[2] = e2;
       }
       named_bar(1, NT);
     }
   }
 
-  // multi-launch mode: persist the running read-out state for the next launch
-  if (multi && !stopped && cta == 0 && tid == 0) {
-    stg_state[ST_A] = stA;
-    stg_state[ST_B] = stB;
-    stg_state[ST_BPREV] = stBp;
+  if (final_t >= 0) {
+    // ---------------- final phase: returned v to the user buffer, then the fp64 read-out
+    // W_hat = eps (a^T log u + b^T log v) of the returned state
+    int64_t u0, u1, v0, v1;
+    cta_rows(A.rows[0], A.gpp, cta, &u0, &u1);
+    cta_rows(A.rows[1], A.gpp, cta, &v0, &v1);
+    float* vdst = A.out[1] + (int64_t)prob * A.wstride[1];
+    const float* udst = A.out[0] + (int64_t)prob * A.wstride[0];
+    if ((final_t ^ A.T) & 1) {
+      const float* src = A.vbuf1 + (int64_t)prob * A.wstride[1];
+      for (int64_t i = v0 + tid; i < v1; i += NT) vdst[i] = __ldcg(src + i);
+    }
+    named_bar(1, NT);
+    const float* ap = A.w[0] + (int64_t)prob * A.wstride[0];
+    const float* bp = A.w[1] + (int64_t)prob * A.wstride[1];
+    double la = 0.0, lb = 0.0;
+    for (int64_t i = u0 + tid; i < u1; i += NT) la += (double)ap[i] * log((double)__ldcg(udst + i));
+    for (int64_t i = v0 + tid; i < v1; i += NT) lb += (double)bp[i] * log((double)__ldcg(vdst + i));
+    la = warp_sum_f64(la);
+    lb = warp_sum_f64(lb);
+    if (lane == 0) {
+      S.xs[0][warp] = la;
+      S.xs[1][warp] = lb;
+    }
+    named_bar(1, NT);
+    if (tid == 0) {
+      la = 0.0;
+      lb = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        la += S.xs[0][w];
+        lb += S.xs[1][w];
+      }
+    }
+    if (A.gpp > 1) {
+      if (tid == 0) {
+        part[cta] = la;
+        part[A.gpp + cta] = lb;
+      }
+      group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (cta == 0 && tid == 0) {
+        la = 0.0;
+        lb = 0.0;
+        for (int c = 0; c < A.gpp; ++c) {
+          la += __ldcg(part + c);
+          lb += __ldcg(part + A.gpp + c);
+        }
+      }
+    }
+    if (cta == 0 && tid == 0) {
+      stg_state[ST_ITERS] = (double)final_t;
+      stg_state[ST_FINAL_A] = la;
+      stg_state[ST_FINAL_B] = lb;
+      stg_state[ST_ROT] = A.eps * (la + lb);
+      stg_state[ST_ERR] = ferr;
+      stg_state[ST_CONV] = (double)conv;
+      stg_state[ST_BRK] = stBrk;
+      __threadfence();
+      stg_state[ST_STOP] = 1.0;
+    }
+  } else if (multi && cta == 0 && tid == 0) {
+    // multi-launch mode: persist the running state for the next launch
     stg_state[ST_ERR] = stErr;
     stg_state[ST_BRK] = stBrk;
   }
@@ -551,7 +634,7 @@ void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv) {
   while (p2 < v) p2 <<= 1;
   *nv = p2;
   if (implicit) {
-    *tr = 8 / p2 > 0 ? 8 / p2 : 1;
+    *tr = 4 / p2 > 0 ? 4 / p2 : 1;   // two tiles of regenerated features live in registers
   } else if (p2 == 1) {
     int t = 8192 / (r > 0 ? r : 1);
     int tt = 32;
@@ -605,7 +688,7 @@ cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool coop, int gri
 #undef X
   } else {
 #define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && a.d == D_) return launch_t<true, NV_, TR_, D_>(a, coop, grid, smem, s);
-    LSK_IMPL_D(X, 1, 8) LSK_IMPL_D(X, 2, 4) LSK_IMPL_D(X, 4, 2)
+    LSK_IMPL_D(X, 1, 4) LSK_IMPL_D(X, 2, 2) LSK_IMPL_D(X, 4, 1)
 #undef X
   }
   return cudaErrorInvalidConfiguration;
@@ -620,7 +703,7 @@ int sinkhorn_max_ctas_per_sm(bool implicit, int r, int d, size_t smem) {
 #undef X
   } else {
 #define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && d == D_) return occupancy_t<true, NV_, TR_, D_>(smem);
-    LSK_IMPL_D(X, 1, 8) LSK_IMPL_D(X, 2, 4) LSK_IMPL_D(X, 4, 2)
+    LSK_IMPL_D(X, 1, 4) LSK_IMPL_D(X, 2, 2) LSK_IMPL_D(X, 4, 1)
 #undef X
   }
   return 0;

@@ -1,0 +1,39 @@
+"""Kernel-time sweep for tuning: times lsk_factored_sinkhorn(_implicit) only (CUDA events)."""
+import argparse, os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2006_07057_b200 as L
+import synth
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--variant", default="stream")
+ap.add_argument("--T", type=int, default=100)
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--cps", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+cfg = synth.get_config(a.config)
+prob = synth.make_problem(cfg, n=a.n, m=a.n)
+X, Y, A_, B_ = (torch.from_numpy(prob[k]).cuda() for k in ("X", "Y", "a", "b"))
+n, m, r, d = X.shape[0], Y.shape[0], cfg.r, cfg.d
+p = L.lsk_feature_params_init(cfg.eps, d, r, 0.0, cfg.anchor_seed, X, Y)
+U = torch.empty((r, d), device="cuda"); L.lsk_draw_anchors(p, U)
+u = torch.empty(n, device="cuda"); v = torch.empty(m, device="cuda")
+opts = L.make_opts(a.T, 0.0, False, a.cps)
+if a.variant == "stream":
+    Xi = torch.empty((n, r), device="cuda"); Ze = torch.empty((m, r), device="cuda")
+    L.lsk_feature_map(p, U, X, Xi); L.lsk_feature_map(p, U, Y, Ze)
+    run = lambda: L.lsk_factored_sinkhorn(Xi, Ze, A_, B_, cfg.eps, opts, u, v, report=False)
+else:
+    run = lambda: L.lsk_factored_sinkhorn_implicit(p, U, X, Y, A_, B_, opts, u, v, report=False)
+run(); torch.cuda.synchronize()
+ts = []
+for _ in range(a.reps):
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); run(); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
+ms = min(ts)
+passes = 2 * a.T + 1
+bytes_ = 4.0 * r * (n + a.T * (n + m))
+print(json.dumps(dict(variant=a.variant, n=n, r=r, T=a.T, env={k: os.environ.get(k) for k in ("LSK_GPP", "LSK_NSTAGE")},
+                      cps=a.cps, ms=round(ms, 3), us_per_pass=round(1e3 * ms / passes, 2),
+                      GBs=round(bytes_ / ms / 1e6), it_s=round(a.T / ms * 1e3))))
