@@ -200,7 +200,7 @@ def run_lsk(args):
     cfg = synth.get_config(args.config)
     variant = args.variant
     if variant == "auto":
-        variant = "implicit" if cfg.d <= 8 else "stream"
+        variant = "stream"   # measured faster on configs 2-4
     n_loc, m_loc = cfg.n, cfg.m
     # weak scaling: the global problem has ws x the per-GPU rows; each rank owns one shard
     full = synth.make_problem(cfg, n=cfg.n * ws, m=cfg.m * ws)

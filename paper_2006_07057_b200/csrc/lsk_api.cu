@@ -180,35 +180,33 @@ struct SolveCfg {
   bool coop = false;
 };
 
-static lsk_status plan_solve(const SinkArgs& A, bool impl, int batch, const lsk_solve_opts* o,
+static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_opts* o,
                              SolveCfg* c) {
-  int tr, nv;
-  sinkhorn_tile_config(A.r, impl, &tr, &nv);
-  if (nv > (impl ? 4 : 8)) return fail(LSK_EDIM, "r too large for this variant");
   c->impl = impl;
   c->batch = batch;
   const int hdr = 64 + 32 * 16;
-  int sf = hdr + (impl ? 0 : tr * A.r);
-  sf = (sf + 31) & ~31;
-  c->stage_floats = sf;
   int cps = (o && o->ctas_per_sm > 0) ? o->ctas_per_sm : (impl ? 2 : (batch > 1 ? 2 : 1));
   const size_t static_smem = sinkhorn_static_smem();
   const size_t smem_sm = 227 * 1024;   // B200: 228 KB per SM, 227 KB usable per CTA
-  const size_t per_cta = std::min<size_t>(max_smem_optin(), smem_sm / cps - 1024);
-  const size_t stage_bytes = (size_t)sf * 4;
-  int nst = (int)((per_cta - static_smem - 512) / stage_bytes);
-  nst = std::min(nst, impl ? 8 : 16);
-  if (nst < 3) {
-    cps = 1;
-    nst = (int)((std::min<size_t>(max_smem_optin(), smem_sm) - static_smem - 512) / stage_bytes);
-    nst = std::min(nst, 16);
-    if (nst < 3) return fail(LSK_EDIM, "r too large: three ring stages do not fit in shared memory");
+  int tr = 0, nv = 0, nst = 0, sf = 0;
+  for (;; cps = 1) {
+    const size_t per_cta =
+        std::min<size_t>(max_smem_optin(), smem_sm / cps - (cps > 1 ? 1024 : 0)) - static_smem - 512;
+    sinkhorn_tile_config(A.r, impl, (int)(per_cta / 3), &tr, &nv);
+    sf = (hdr + (impl ? 0 : tr * A.r) + 31) & ~31;
+    nst = std::min<int>((int)(per_cta / ((size_t)sf * 4)), impl ? 8 : 16);
+    if (nst >= 3 || cps == 1) break;
   }
+  if (nv > (impl ? 4 : 8)) return fail(LSK_EDIM, "r too large for this variant");
   // the pipelined tile loop holds two stages while the producer fills a third
+  if (nst < 3) return fail(LSK_EDIM, "r too large: three ring stages do not fit in shared memory");
   if (const char* e = getenv("LSK_NSTAGE")) nst = std::max(3, std::min(nst, atoi(e)));   // tuning knob
+  A.tr = tr;
+  A.nv = nv;
+  c->stage_floats = sf;
   c->nstage = nst;
-  c->smem = (size_t)nst * stage_bytes;
-  int occ = sinkhorn_max_ctas_per_sm(impl, A.r, A.d, c->smem);
+  c->smem = (size_t)nst * sf * 4;
+  int occ = sinkhorn_max_ctas_per_sm(impl, nv, tr, A.d, c->smem);
   if (occ < 1) return fail(LSK_EUNSUPPORTED, "sinkhorn kernel does not fit on an SM");
   cps = std::min(cps, occ);
   const int sms = num_sms();

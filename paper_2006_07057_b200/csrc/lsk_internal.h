@@ -62,15 +62,17 @@ struct SinkArgs {
   const float* beta2;      // [r]     log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
   float c2;                // -2 log2e / eps
   int dbg;                 // tuning only: 1 = consumers release stages without computing
+  int tr;                  // rows per tile (template dispatch)
+  int nv;                  // float4 column groups per consumer thread (template dispatch)
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.
 cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool cooperative, int grid,
                             size_t smem, cudaStream_t s);
 // Kernel configuration for a given r / mode: rows per tile and stage floats.
-void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv);
+void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, int* nv);
 size_t sinkhorn_static_smem();
-int sinkhorn_max_ctas_per_sm(bool implicit, int r, int d, size_t dyn_smem);
+int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t dyn_smem);
 
 // Feature kernels (lsk_features.cu)
 cudaError_t launch_max_sqnorm(const float* X, int64_t n, int d, unsigned long long* out,

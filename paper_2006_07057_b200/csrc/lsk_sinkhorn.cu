@@ -26,6 +26,8 @@
 // ex2 in registers (expanded form of PAPER.md:934 in base 2).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "lsk_internal.h"
 #include "lsk_ptx.cuh"
@@ -89,14 +91,15 @@ __device__ __forceinline__ double warp_sum_f64(double x) {
 
 // Barrier among the gpp CTAs of one problem: monotone counter, k-th barrier waits for
 // k * gpp arrivals (counter zeroed once per solve by the host).
+// bar.sync orders the CTA's writes before thread 0's gpu-scope release; thread 0's acquire
+// is ordered before the other threads' reads by the second bar.sync (cumulativity) — the
+// same pattern as CUTLASS's GenericBarrier.  Readers use ld.global.cg (L2), so no L1 flush.
 __device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int target, int tid) {
   named_bar(1, NT);
   if (tid == 0) {
-    __threadfence();
     red_release_add(ctr, 1u);
     while (ld_acquire(ctr) < target) {
     }
-    __threadfence();
   }
   named_bar(1, NT);
 }
@@ -368,26 +371,27 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       }
       if (kind != PK_ERR) {
         // vr_l = 0 in lanes >= frows, so tail rows add 0 x (finite stale/zero data)
-        float4 fvv[IMPL ? 1 : TR][IMPL ? 1 : NV];
-        if constexpr (!IMPL) {
+        float vis[TR];
 #pragma unroll
-          for (int i = 0; i < TR; ++i)
+        for (int i = 0; i < TR; ++i) vis[i] = __shfl_sync(0xffffffffu, vr_l, i);
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-              fvv[i][j] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
-        }
+        for (int j = 0; j < NV; ++j) {
+          float4 fvv[IMPL ? 1 : TR];
+          if constexpr (!IMPL) {
 #pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+            for (int i = 0; i < TR; ++i)
+              fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+          }
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
+          for (int i = 0; i < TR; ++i) {
+            const float vi = vis[i];
             if constexpr (IMPL) {
               acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
               acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
               acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
               acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
             } else {
-              const float4 fv = fvv[i][j];
+              const float4 fv = fvv[i];
               acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
               acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
               acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
@@ -457,26 +461,25 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (kind != PK_INIT) {
         // rows >= `rows` of a tail tile hold finite stale/zero data; their dots are unused
         float pr[TR];
-        float4 fvv[IMPL ? 1 : TR][IMPL ? 1 : NV];
-        if constexpr (!IMPL) {
 #pragma unroll
-          for (int i = 0; i < TR; ++i)
+        for (int i = 0; i < TR; ++i) pr[i] = 0.f;
 #pragma unroll
-            for (int j = 0; j < NV; ++j)
-              fvv[i][j] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
-        }
+        for (int j = 0; j < NV; ++j) {
+          float4 fvv[IMPL ? 1 : TR];
+          if constexpr (!IMPL) {
 #pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          pr[i] = 0.f;
+            for (int i = 0; i < TR; ++i)   // all loads of this column group first
+              fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+          }
 #pragma unroll
-          for (int j = 0; j < NV; ++j) {
+          for (int i = 0; i < TR; ++i) {
             if constexpr (IMPL) {
               pr[i] = fmaf(cur[i][j][0], s[j].x, pr[i]);
               pr[i] = fmaf(cur[i][j][1], s[j].y, pr[i]);
               pr[i] = fmaf(cur[i][j][2], s[j].z, pr[i]);
               pr[i] = fmaf(cur[i][j][3], s[j].w, pr[i]);
             } else {
-              const float4 fv = fvv[i][j];
+              const float4 fv = fvv[i];
               pr[i] = fmaf(fv.x, s[j].x, pr[i]);
               pr[i] = fmaf(fv.y, s[j].y, pr[i]);
               pr[i] = fmaf(fv.z, s[j].z, pr[i]);
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 }
 
 // ------------------------------------------------------------------------------------------
-void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv) {
+void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, int* nv) {
   const int r4 = (r + 3) / 4;
   int v = (r4 + NT - 1) / NT;
   int p2 = 1;
@@ -635,14 +638,20 @@ void sinkhorn_tile_config(int r, bool implicit, int* tr, int* nv) {
   *nv = p2;
   if (implicit) {
     *tr = 4 / p2 > 0 ? 4 / p2 : 1;   // two tiles of regenerated features live in registers
-  } else if (p2 == 1) {
-    int t = 8192 / (r > 0 ? r : 1);
-    int tt = 32;
-    while (tt > t && tt > 8) tt >>= 1;
-    *tr = tt;
-  } else {
-    *tr = 8 / p2 > 0 ? 8 / p2 : 1;
+    return;
   }
+  // largest instantiated TR whose stage fits the budget (target 64 KB: long tiles amortise
+  // the per-tile cross-warp exchange; measured on config 2: 32 KB stages 4.6 TB/s, 64 KB
+  // stages 5.3 TB/s)
+  const int lo = std::max(1, 8 / p2), hi = std::max(1, 32 / p2);
+  int tt = hi;
+  const int budget = std::min(max_stage_bytes, 65536 + kHdr * 4);
+  while (tt > lo && (kHdr + tt * r) * 4 > budget) tt >>= 1;
+  if (const char* e = getenv("LSK_TR")) {   // tuning knob
+    const int x = atoi(e);
+    if (x >= lo && x <= hi) tt = x;
+  }
+  *tr = tt;
 }
 
 size_t sinkhorn_static_smem() { return sizeof(Smem); }
@@ -674,14 +683,14 @@ static int occupancy_t(size_t smem) {
   return nb;
 }
 
-#define LSK_STREAM_CASES(X) X(1, 32) X(1, 16) X(1, 8) X(2, 4) X(4, 2) X(8, 1)
+#define LSK_STREAM_CASES(X) X(1, 32) X(1, 16) X(1, 8) X(2, 16) X(2, 8) X(2, 4) X(4, 8) X(4, 4) \
+  X(4, 2) X(8, 4) X(8, 2) X(8, 1)
 #define LSK_IMPL_D(X, NV, TR) X(NV, TR, 1) X(NV, TR, 2) X(NV, TR, 3) X(NV, TR, 4) \
   X(NV, TR, 5) X(NV, TR, 6) X(NV, TR, 7) X(NV, TR, 8)
 
 cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool coop, int grid, size_t smem,
                             cudaStream_t s) {
-  int tr, nv;
-  sinkhorn_tile_config(a.r, implicit, &tr, &nv);
+  const int tr = a.tr, nv = a.nv;
   if (!implicit) {
 #define X(NV_, TR_) if (nv == NV_ && tr == TR_) return launch_t<false, NV_, TR_, 1>(a, coop, grid, smem, s);
     LSK_STREAM_CASES(X)
@@ -694,9 +703,7 @@ cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool coop, int gri
   return cudaErrorInvalidConfiguration;
 }
 
-int sinkhorn_max_ctas_per_sm(bool implicit, int r, int d, size_t smem) {
-  int tr, nv;
-  sinkhorn_tile_config(r, implicit, &tr, &nv);
+int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t smem) {
   if (!implicit) {
 #define X(NV_, TR_) if (nv == NV_ && tr == TR_) return occupancy_t<false, NV_, TR_, 1>(smem);
     LSK_STREAM_CASES(X)

@@ -12,7 +12,34 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--cps", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
+ap2 = None
 cfg = synth.get_config(a.config)
+if a.config == 4:
+    B = int(os.environ.get("SWEEP_BATCH", "256"))
+    n = a.n or cfg.n
+    bp = synth.make_batched(cfg, batch=B, n=n, m=n)
+    X, Y, A_, B_ = (torch.from_numpy(bp[k]).cuda() for k in ("X", "Y", "a", "b"))
+    r, d = cfg.r, cfg.d
+    p = L.lsk_feature_params_init(cfg.eps, d, r, 0.0, cfg.anchor_seed, X.reshape(-1, d), Y.reshape(-1, d))
+    U = torch.empty((r, d), device="cuda"); L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((B, n, r), device="cuda"); Ze = torch.empty((B, n, r), device="cuda")
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(); L.lsk_feature_map_batched(p, U, X, Xi); L.lsk_feature_map_batched(p, U, Y, Ze); f1.record()
+    torch.cuda.synchronize()
+    u = torch.empty((B, n), device="cuda"); v = torch.empty((B, n), device="cuda")
+    opts = L.make_opts(a.T, 0.0, False, a.cps)
+    run = lambda: L.lsk_factored_sinkhorn_batched(Xi, Ze, A_, B_, cfg.eps, opts, u, v, report=False)
+    run(); torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); run(); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
+    ms = min(ts)
+    bytes_ = 4.0 * r * B * (n + a.T * 2 * n)
+    print(json.dumps(dict(variant="batched", B=B, n=n, r=r, T=a.T, feature_map_ms=round(f0.elapsed_time(f1), 3),
+                          ms=round(ms, 3), GBs=round(bytes_ / ms / 1e6), it_s=round(a.T / ms * 1e3))))
+    sys.exit(0)
 prob = synth.make_problem(cfg, n=a.n, m=a.n)
 X, Y, A_, B_ = (torch.from_numpy(prob[k]).cuda() for k in ("X", "Y", "a", "b"))
 n, m, r, d = X.shape[0], Y.shape[0], cfg.r, cfg.d
