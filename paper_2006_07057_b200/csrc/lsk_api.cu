@@ -180,8 +180,38 @@ struct SolveCfg {
   bool coop = false;
 };
 
+static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o, SolveCfg* c) {
+  if (A.r > 4096) return fail(LSK_EDIM, "implicit variant supports r <= 4096");
+  int nt, nv, tr;
+  implicit_config(A.r, &nt, &nv, &tr);
+  A.tr = tr;
+  A.nv = nv;
+  c->impl = true;
+  c->batch = batch;
+  c->smem = 0;
+  c->nstage = 0;
+  c->stage_floats = 0;
+  int occ = implicit_max_ctas_per_sm(A.r, A.d);
+  if (occ < 1) return fail(LSK_EUNSUPPORTED, "implicit kernel does not fit on an SM");
+  int cps = (o && o->ctas_per_sm > 0) ? std::min(o->ctas_per_sm, occ) : occ;
+  if (batch > 1) {
+    c->gpp = 1;
+    c->grid = batch;
+    c->coop = false;
+  } else {
+    const int64_t rows = std::max(A.rows[0], A.rows[1]);
+    const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
+    c->gpp = (int)std::min<int64_t>((int64_t)num_sms() * cps, want);
+    if (const char* e = getenv("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
+    c->grid = c->gpp;
+    c->coop = c->gpp > 1;
+  }
+  return LSK_OK;
+}
+
 static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_opts* o,
                              SolveCfg* c) {
+  if (impl) return plan_implicit(A, batch, o, c);
   c->impl = impl;
   c->batch = batch;
   const int hdr = 64 + 32 * 16;
@@ -237,6 +267,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.num_passes = 2 * A.T + 1 + A.want_err;
   SolveCfg c;
   LSK_TRY(plan_solve(A, impl, batch, o, &c));
+  if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   if (comm && c.gpp < 2) {
     // the multi-launch path needs svec: force >= 2 CTAs
     c.gpp = std::min(2, num_sms());
@@ -255,12 +286,19 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.bar = reinterpret_cast<unsigned int*>(ws + cv.take(sizeof(unsigned int) * batch));
   A.vbuf1 = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * A.rows[1] * batch));
   LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles * batch, s));
+  unsigned long long* trace = nullptr;
+  const char* trace_path = getenv("LSK_TRACE");   // tuning only: per-pass barrier timestamps
+  if (trace_path && batch == 1) {
+    cudaMalloc(&trace, sizeof(unsigned long long) * 4 * (size_t)A.num_passes * c.gpp);
+    cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 4 * (size_t)A.num_passes * c.gpp, s);
+  }
+  A.trace = trace;
   if (!comm) {
     A.pass_begin = 0;
     A.pass_end = A.num_passes;
     A.multi_launch = 0;
     LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
-    LSK_CU(launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+    LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
   } else {
     if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
     A.multi_launch = 1;
@@ -269,7 +307,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       A.pass_end = std::min(p + 1, A.num_passes);
       if (p == A.num_passes) A.pass_end = p;   // finalise-only launch
       LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
-      LSK_CU(launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+      LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
       if (p < A.num_passes)
         LSK_TRY(nccl_check(nccl().allReduce(A.svec, A.svec, (size_t)rs * batch, ncclFloat64,
                                             ncclSum, comm->comm, s),
@@ -279,6 +317,18 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     LSK_TRY(nccl_check(nccl().allReduce(A.state + ST_FINAL_A, A.state + ST_FINAL_A, 2,
                                         ncclFloat64, ncclSum, comm->comm, s),
                        "ncclAllReduce(read-out)"));
+  }
+  if (trace) {
+    std::vector<unsigned long long> h(4 * (size_t)A.num_passes * c.gpp);
+    cudaMemcpyAsync(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      int hdr[2] = {A.num_passes, c.gpp};
+      fwrite(hdr, sizeof(int), 2, fp);
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      fclose(fp);
+    }
+    cudaFree(trace);
   }
   if (reps) {
     std::vector<double> st((size_t)kStateDoubles * batch);

@@ -1,0 +1,512 @@
+// lsk_implicit.cu — Alg. 1 on K_theta = xi zeta^T WITHOUT materialising
+// the factors: every pass regenerates F_jk = phi(p_j, u_k)/sqrt(r) in registers from the
+// point rows and the anchors (Lemma decomp-RBF, expanded in base 2):
+//     F_jk = 2^( alpha2_j + beta2_k + sum_c W_kc p_jc ),
+//     alpha2_j = -(2 log2e/eps)|p_j|^2, W_kc = (4 log2e/eps) U_kc,
+//     beta2_k = log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
+// so a pass costs one MUFU ex2 + (d+3) FFMA-pipe ops per entry and ~(4d+12) bytes per row.
+//
+// Layout: one CTA per SM made of TEAMS independent teams of TS threads (all consumers, no
+// producer warp: 512 threads x 128 registers).  A team owns every column: thread t of a
+// team owns float4 column groups {t, t+TS, ...} (its W, beta2, slice of s and accumulators
+// live in registers).  The teams take alternate tiles of the CTA's rows, each with its own
+// loader warp (cp.async two tiles ahead into a 4-slot ring) and its own named barrier, so
+// while one team waits on its per-tile row-dot exchange the other team issues MUFU work.
+// The two teams' fp64 partials are added in a fixed order at the end of the pass.  Pass
+// boundary, stopping test and the fp64 read-out are those of the streaming kernel.
+#include <algorithm>
+#include <cmath>
+
+#include "lsk_internal.h"
+#include "lsk_ptx.cuh"
+#include "lsk_sink_common.cuh"
+
+namespace lsk {
+
+namespace impl {
+
+constexpr int kRing = 4;            // tile slots (two tiles in flight ahead of the current)
+constexpr int kSlot = 64 + 32 * 8;  // floats per slot: c[32], vold[32], x[32][8]
+
+template <int TS, int TEAMS>
+struct Smem {
+  float slot[TEAMS][kRing][kSlot];
+  float red[TEAMS][2][TS / 32][32];
+  double xs[2][TS * TEAMS / 32];
+  double ext[kExtra];
+};
+
+template <int TS, int TEAMS, int NV, int TR, int D>
+__global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs A) {
+  constexpr int NT = TS * TEAMS;       // CTA threads
+  constexpr int NWT = TS / 32;         // warps per team
+  constexpr int NW = NT / 32;
+  constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;
+  static_assert(TEAMS == 1 || TEAMS == 2, "1 or 2 teams");
+  __shared__ __align__(16) Smem<TS, TEAMS> S;
+  __shared__ double comb[TEAMS > 1 ? TS : 1][TEAMS > 1 ? NV * 4 : 1];
+
+  const int tid = threadIdx.x;
+  const int team = tid / TS, ttid = tid - team * TS;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int twarp = ttid >> 5;          // warp index within the team
+  const uint32_t team_bar = 2u + (uint32_t)team;
+  const int prob = blockIdx.x / A.gpp;
+  const int cta = blockIdx.x - prob * A.gpp;
+  const int r = A.r;
+  double* stg_state = A.state + (int64_t)prob * kStateDoubles;
+  if (__ldcg(stg_state + ST_STOP) != 0.0) return;   // finished (multi-launch mode)
+
+  // per-thread anchor constants for the owned column groups
+  const int R4 = r >> 2;
+  int g[NV];
+  bool gv[NV];
+  float4 Wr[NV][D];
+  float4 b2[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    g[j] = ttid + j * TS;
+    gv[j] = g[j] < R4;
+    if (gv[j]) {
+      b2[j] = *reinterpret_cast<const float4*>(A.beta2 + 4 * g[j]);
+#pragma unroll
+      for (int c = 0; c < D; ++c) Wr[j][c] = *reinterpret_cast<const float4*>(A.Wt + (int64_t)c * r + 4 * g[j]);
+    } else {   // padding groups produce exact zeros: ex2(-inf) = 0
+      b2[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+      for (int c = 0; c < D; ++c) Wr[j][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  for (int i = tid; i < TEAMS * kRing * kSlot; i += NT) (&S.slot[0][0][0])[i] = 0.f;
+  __syncthreads();
+
+  float4 s[NV];
+  double acc64[NV][4];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+  }
+
+  double stErr = __ldcg(stg_state + ST_ERR);
+  double stBrk = __ldcg(stg_state + ST_BRK);
+  const int64_t rstride = r + kExtra;
+  double* part = A.part + (int64_t)prob * rstride * A.gpp;
+  double* svec = A.svec + (int64_t)prob * rstride;
+  const bool multi = A.multi_launch != 0;
+  unsigned int nbar = 0;
+  int final_t = -1, conv = 0;
+  double ferr = -1.0;
+
+  for (int p = A.pass_begin;; ++p) {
+    // ---------------- results of pass q = p-1: stopping test (see lsk_sinkhorn.cu) -------
+    const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
+    if (have_prev) {
+      const int q = p - 1;
+      const int qk = pass_kind(q, A);
+      double e_err, e_brk;
+      if (A.gpp > 1) {
+        e_err = __ldcg(svec + r);
+        e_brk = __ldcg(svec + r + 1);
+      } else {
+        e_err = S.ext[0];
+        e_brk = S.ext[1];
+      }
+      stBrk += e_brk;
+      if (qk == PK_V) {
+        const int t = (q + 1) / 2;
+        if (t >= 2) {
+          stErr = e_err;
+          if (A.tol_mode && e_err < A.tol) {
+            final_t = t - 1;
+            ferr = e_err;
+            conv = 1;
+          }
+        }
+      } else if (qk == PK_ERR) {
+        stErr = e_err;
+      }
+      if (final_t < 0 && q == A.num_passes - 1) {
+        final_t = A.T;
+        ferr = A.want_err ? stErr : -1.0;
+        conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
+      }
+      if (final_t >= 0) break;
+    }
+    if (p >= A.pass_end) break;
+
+    // ---------------- pass p ---------------------------------------------------------------
+    const int kind = pass_kind(p, A);
+    if (kind == PK_NONE) continue;
+    const int f = (kind == PK_V || kind == PK_ERR) ? 1 : 0;
+    if (kind != PK_INIT) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (!gv[j]) {
+          s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (A.gpp > 1) {
+          const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j]));
+          const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j] + 2));
+          s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+        } else {   // gpp == 1: the combined accumulator is in team 0 (and in comb for team 1)
+          if constexpr (TEAMS > 1) {
+            if (team == 1)
+              s[j] = make_float4((float)comb[ttid][j * 4], (float)comb[ttid][j * 4 + 1],
+                                 (float)comb[ttid][j * 4 + 2], (float)comb[ttid][j * 4 + 3]);
+            else
+              s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
+          } else {
+            s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
+          }
+        }
+      }
+      if constexpr (TEAMS > 1) named_bar(1, NT);   // comb reads done before it is rewritten
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+
+    int64_t r0, r1;
+    cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
+    const int ntiles_cta = (int)((r1 - r0 + TR - 1) / TR);
+    const int ntiles = (ntiles_cta - team + TEAMS - 1) / TEAMS;   // this team: tiles team, team+TEAMS, ...
+    const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
+    const float* Xp = A.X[f] + (int64_t)prob * A.fstride[f];
+    const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
+    const float* vold = need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) : nullptr;
+    float* outp = nullptr;
+    if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
+    if (kind == PK_V) outp = vbuf_ptr(A, prob, (p + 1) / 2);
+    double errsum = 0.0, brksum = 0.0;
+    float4 acc32[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int tiles_since_flush = 0;
+
+    // warp 0 stages tile t (point rows + c_j + v_old_j) into slot t % kRing.  v_old_j was
+    // written by this same lane two passes earlier (same tiling), so no extra ordering.
+    auto issue = [&](int t) {
+      if (t < ntiles) {
+        const int64_t row0 = r0 + (int64_t)(team + t * TEAMS) * TR;
+        const int rows = (int)min((int64_t)TR, r1 - row0);
+        float* sl = S.slot[team][t % kRing];
+        if (lane < rows) {
+          cp_async4(sl + lane, wp + row0 + lane);
+          if (need_vold) cp_async4(sl + 32 + lane, vold + row0 + lane);
+#pragma unroll
+          for (int c = 0; c < D; ++c) cp_async4(sl + 64 + lane * 8 + c, Xp + (row0 + lane) * D + c);
+        }
+      }
+      cp_async_commit();
+    };
+    if (twarp == 0) {
+      issue(0);
+      issue(1);
+      cp_async_wait<1>();
+    }
+    named_bar(team_bar, TS);
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t row0 = r0 + (int64_t)(team + t * TEAMS) * TR;
+      const int rows = (int)min((int64_t)TR, r1 - row0);
+      const float* sl = S.slot[team][t % kRing];
+      if (twarp == 0) issue(t + 2);   // slot (t+2)%4 was last read in tile t-2 (< previous barrier)
+
+      // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero data)
+      float fr[TR][NV][4];
+#pragma unroll
+      for (int i = 0; i < TR; ++i) {
+        float x[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[c] = sl[64 + i * 8 + c];
+        float al = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
+        al *= A.c2;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          float e0 = al + b2[j].x, e1 = al + b2[j].y, e2 = al + b2[j].z, e3 = al + b2[j].w;
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            e0 = fmaf(Wr[j][c].x, x[c], e0);
+            e1 = fmaf(Wr[j][c].y, x[c], e1);
+            e2 = fmaf(Wr[j][c].z, x[c], e2);
+            e3 = fmaf(Wr[j][c].w, x[c], e3);
+          }
+          fr[i][j][0] = ex2(e0);
+          fr[i][j][1] = ex2(e1);
+          fr[i][j][2] = ex2(e2);
+          fr[i][j][3] = ex2(e3);
+        }
+      }
+      const int rb = t & 1;
+      if (kind != PK_INIT) {
+        float pr[TR];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          pr[i] = 0.f;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            pr[i] = fmaf(fr[i][j][0], s[j].x, pr[i]);
+            pr[i] = fmaf(fr[i][j][1], s[j].y, pr[i]);
+            pr[i] = fmaf(fr[i][j][2], s[j].z, pr[i]);
+            pr[i] = fmaf(fr[i][j][3], s[j].w, pr[i]);
+          }
+        }
+        const float tot = warp_transpose_reduce<TR>(pr, lane);
+        constexpr int kLanesPerRow = 32 / TR;
+        if ((lane & (kLanesPerRow - 1)) == 0) S.red[team][rb][twarp][lane / kLanesPerRow] = tot;
+      }
+      if (twarp == 0) cp_async_wait<1>();   // tile t+1 has landed (only t+2 may be pending)
+      named_bar(team_bar, TS);               // publishes red[rb] and slot (t+1) to the team
+
+      float vr_l = 0.f;
+      if (kind == PK_INIT) {
+        vr_l = (lane < rows) ? 1.f : 0.f;   // u^0 = 1 (reading C6)
+      } else if (lane < rows) {
+        float tt = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWT; ++w) tt += S.red[team][rb][w][lane];   // fixed order
+        const float c = sl[lane];
+        if (kind != PK_ERR) vr_l = __fdiv_rn(c, tt);
+        if (twarp == 0) {
+          if (kind == PK_ERR || (kind == PK_V && p >= 3))
+            errsum += fabs((double)sl[32 + lane] * (double)tt - (double)c);
+          if (kind != PK_ERR) {
+            if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
+            outp[row0 + lane] = vr_l;
+          }
+        }
+      }
+      if (kind != PK_ERR) {
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
+            acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
+            acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
+            acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
+          }
+        }
+        if (++tiles_since_flush == kFlushTiles) {
+          tiles_since_flush = 0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            acc64[j][0] += (double)acc32[j].x;
+            acc64[j][1] += (double)acc32[j].y;
+            acc64[j][2] += (double)acc32[j].z;
+            acc64[j][3] += (double)acc32[j].w;
+            acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+    }
+    if (twarp == 0) cp_async_wait<0>();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc64[j][0] += (double)acc32[j].x;
+      acc64[j][1] += (double)acc32[j].y;
+      acc64[j][2] += (double)acc32[j].z;
+      acc64[j][3] += (double)acc32[j].w;
+    }
+
+    // ---------------- end of pass: teams combined (fixed order), cross-CTA fp64 reduction ---
+    double e0 = 0.0, e1 = 0.0;
+    if (twarp == 0) {
+      e0 = warp_sum_f64(errsum);
+      e1 = warp_sum_f64(brksum);
+    }
+    if constexpr (TEAMS > 1) {
+      if (team == 1) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) comb[ttid][j * 4 + q] = acc64[j][q];
+        if (ttid == 0) {
+          S.xs[0][0] = e0;
+          S.xs[1][0] = e1;
+        }
+      }
+      named_bar(1, NT);
+      if (team == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc64[j][q] += comb[ttid][j * 4 + q];
+        if (ttid == 0) {
+          e0 += S.xs[0][0];
+          e1 += S.xs[1][0];
+        }
+      }
+      named_bar(1, NT);
+    }
+    unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
+    if (trc) trc[0] = globaltimer();
+    if (A.gpp > 1) {
+      if (team == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (gv[j]) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[(int64_t)(4 * g[j] + q) * A.gpp + cta] = acc64[j][q];
+          }
+        }
+      }
+      if (tid == 0) {
+        part[(int64_t)(r + 0) * A.gpp + cta] = e0;
+        part[(int64_t)(r + 1) * A.gpp + cta] = e1;
+        part[(int64_t)(r + 2) * A.gpp + cta] = 0.0;
+        part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
+      }
+      group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (trc) trc[1] = globaltimer();
+      for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NW) {
+        const double* col = part + (int64_t)k * A.gpp;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
+        acc = warp_sum_f64(acc);
+        if (lane == 0) svec[k] = acc;
+      }
+      if (trc) trc[2] = globaltimer();
+      if (!multi) group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (trc) trc[3] = globaltimer();
+    } else {
+      if constexpr (TEAMS > 1) {
+        if (team == 0) {
+#pragma unroll
+          for (int j = 0; j < NV; ++j)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) comb[ttid][j * 4 + q] = acc64[j][q];
+        }
+      }
+      if (tid == 0) {
+        S.ext[0] = e0;
+        S.ext[1] = e1;
+      }
+      named_bar(1, NT);
+    }
+  }
+
+  if (final_t >= 0) {
+    // returned v into the user buffer, then W_hat = eps (a^T log u + b^T log v) in fp64
+    int64_t u0, u1, v0, v1;
+    cta_rows(A.rows[0], A.gpp, cta, &u0, &u1);
+    cta_rows(A.rows[1], A.gpp, cta, &v0, &v1);
+    float* vdst = A.out[1] + (int64_t)prob * A.wstride[1];
+    const float* udst = A.out[0] + (int64_t)prob * A.wstride[0];
+    if ((final_t ^ A.T) & 1) {
+      const float* src = A.vbuf1 + (int64_t)prob * A.wstride[1];
+      for (int64_t i = v0 + tid; i < v1; i += NT) vdst[i] = __ldcg(src + i);
+    }
+    named_bar(1, NT);
+    const float* ap = A.w[0] + (int64_t)prob * A.wstride[0];
+    const float* bp = A.w[1] + (int64_t)prob * A.wstride[1];
+    double la = 0.0, lb = 0.0;
+    for (int64_t i = u0 + tid; i < u1; i += NT) la += (double)ap[i] * log((double)__ldcg(udst + i));
+    for (int64_t i = v0 + tid; i < v1; i += NT) lb += (double)bp[i] * log((double)__ldcg(vdst + i));
+    la = warp_sum_f64(la);
+    lb = warp_sum_f64(lb);
+    if (lane == 0) {
+      S.xs[0][warp] = la;
+      S.xs[1][warp] = lb;
+    }
+    named_bar(1, NT);
+    if (tid == 0) {
+      la = 0.0;
+      lb = 0.0;
+      for (int w = 0; w < NW; ++w) {
+        la += S.xs[0][w];
+        lb += S.xs[1][w];
+      }
+    }
+    if (A.gpp > 1) {
+      if (tid == 0) {
+        part[cta] = la;
+        part[A.gpp + cta] = lb;
+      }
+      group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (cta == 0 && tid == 0) {
+        la = 0.0;
+        lb = 0.0;
+        for (int c = 0; c < A.gpp; ++c) {
+          la += __ldcg(part + c);
+          lb += __ldcg(part + A.gpp + c);
+        }
+      }
+    }
+    if (cta == 0 && tid == 0) {
+      stg_state[ST_ITERS] = (double)final_t;
+      stg_state[ST_FINAL_A] = la;
+      stg_state[ST_FINAL_B] = lb;
+      stg_state[ST_ROT] = A.eps * (la + lb);
+      stg_state[ST_ERR] = ferr;
+      stg_state[ST_CONV] = (double)conv;
+      stg_state[ST_BRK] = stBrk;
+      __threadfence();
+      stg_state[ST_STOP] = 1.0;
+    }
+  } else if (multi && cta == 0 && tid == 0) {
+    stg_state[ST_ERR] = stErr;
+    stg_state[ST_BRK] = stBrk;
+  }
+}
+
+}  // namespace impl
+
+// (TS, TEAMS, NV, TR) per r: r <= 1024 -> (256, 2, 1, 8); r <= 2048 -> (512, 1, 1, 8);
+// r <= 4096 -> (512, 1, 2, 2).  Always 512 threads, one CTA per SM.
+void implicit_config(int r, int* nt, int* nv, int* tr) {
+  const int r4 = (r + 3) / 4;
+  if (r4 <= 256) { *nt = 256; *nv = 1; *tr = 8; }
+  else if (r4 <= 512) { *nt = 512; *nv = 1; *tr = 8; }
+  else { *nt = 512; *nv = 2; *tr = 2; }
+}
+
+#define LSK_IMPL2(X, TS, TM, NV, TR) X(TS, TM, NV, TR, 1) X(TS, TM, NV, TR, 2) \
+  X(TS, TM, NV, TR, 3) X(TS, TM, NV, TR, 4) X(TS, TM, NV, TR, 5) X(TS, TM, NV, TR, 6)     \
+  X(TS, TM, NV, TR, 7) X(TS, TM, NV, TR, 8)
+#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 512, 1, 1, 8) \
+  LSK_IMPL2(X, 512, 1, 2, 2)
+
+cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
+  int ts, nv, tr;
+  implicit_config(a.r, &ts, &nv, &tr);
+#define X(TS_, TM_, NV_, TR_, D_)                                                              \
+  if (ts == TS_ && nv == NV_ && tr == TR_ && a.d == D_) {                                      \
+    auto kern = impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>;                                 \
+    cudaError_t e;                                                                             \
+    if (coop) {                                                                                \
+      void* args[] = {(void*)&a};                                                              \
+      e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS_ * TM_), args, 0, s); \
+    } else {                                                                                   \
+      kern<<<grid, TS_ * TM_, 0, s>>>(a);                                                      \
+      e = cudaGetLastError();                                                                  \
+    }                                                                                          \
+    count_launch();                                                                            \
+    return e;                                                                                  \
+  }
+  LSK_IMPL2_ALL(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+
+int implicit_max_ctas_per_sm(int r, int d) {
+  int ts, nv, tr;
+  implicit_config(r, &ts, &nv, &tr);
+#define X(TS_, TM_, NV_, TR_, D_)                                                              \
+  if (ts == TS_ && nv == NV_ && tr == TR_ && d == D_) {                                        \
+    int nb = 0;                                                                                \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>, TS_ * TM_, 0); \
+    return nb;                                                                                 \
+  }
+  LSK_IMPL2_ALL(X)
+#undef X
+  return 0;
+}
+
+}  // namespace lsk

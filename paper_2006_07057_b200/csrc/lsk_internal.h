@@ -62,6 +62,7 @@ struct SinkArgs {
   const float* beta2;      // [r]     log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
   float c2;                // -2 log2e / eps
   int dbg;                 // tuning only: 1 = consumers release stages without computing
+  unsigned long long* trace;   // tuning only: [pass][cta][4] globaltimer stamps, or NULL
   int tr;                  // rows per tile (template dispatch)
   int nv;                  // float4 column groups per consumer thread (template dispatch)
 };
@@ -73,6 +74,11 @@ cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool cooperative, 
 void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, int* nv);
 size_t sinkhorn_static_smem();
 int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t dyn_smem);
+
+// Implicit (recompute) kernel (lsk_implicit.cu): all-consumer CTAs, no dynamic smem.
+void implicit_config(int r, int* nt, int* nv, int* tr);
+cudaError_t launch_implicit(const SinkArgs& a, bool cooperative, int grid, cudaStream_t s);
+int implicit_max_ctas_per_sm(int r, int d);
 
 // Feature kernels (lsk_features.cu)
 cudaError_t launch_max_sqnorm(const float* X, int64_t n, int d, unsigned long long* out,

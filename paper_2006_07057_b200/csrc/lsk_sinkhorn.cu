@@ -31,6 +31,7 @@
 
 #include "lsk_internal.h"
 #include "lsk_ptx.cuh"
+#include "lsk_sink_common.cuh"
 
 namespace lsk {
 
@@ -49,64 +50,6 @@ struct Smem {
   int done_pass;
   int stop;
 };
-
-__device__ __forceinline__ int pass_kind(int p, const SinkArgs& A) {
-  if (p == 0) return PK_INIT;
-  if (p <= 2 * A.T) return (p & 1) ? PK_V : PK_U;
-  if (p == 2 * A.T + 1 && A.want_err) return PK_ERR;
-  return PK_NONE;
-}
-
-__device__ __forceinline__ void cta_rows(int64_t total, int gpp, int cta, int64_t* r0,
-                                         int64_t* r1) {
-  *r0 = (total * cta) / gpp;
-  *r1 = (total * (cta + 1)) / gpp;
-}
-
-// Warp transpose-reduce: each lane holds v[0..TR) (one partial per row).  Returns, in every
-// lane, the warp total of row (lane >> (5 - log2 TR)).  Fixed shuffle pattern: deterministic.
-template <int TR>
-__device__ __forceinline__ float warp_transpose_reduce(float (&v)[TR], int lane) {
-#pragma unroll
-  for (int w = TR / 2, off = 16; w >= 1; w >>= 1, off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = upper ? v[i] : v[i + w];
-      const float keep = upper ? v[i + w] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-  constexpr int kLog = (TR >= 32) ? 5 : (TR >= 16) ? 4 : (TR >= 8) ? 3 : (TR >= 4) ? 2 : (TR >= 2) ? 1 : 0;
-#pragma unroll
-  for (int off = 16 >> kLog; off >= 1; off >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
-  return v[0];
-}
-
-__device__ __forceinline__ double warp_sum_f64(double x) {
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-  return x;
-}
-
-// Barrier among the gpp CTAs of one problem: monotone counter, k-th barrier waits for
-// k * gpp arrivals (counter zeroed once per solve by the host).
-// bar.sync orders the CTA's writes before thread 0's gpu-scope release; thread 0's acquire
-// is ordered before the other threads' reads by the second bar.sync (cumulativity) — the
-// same pattern as CUTLASS's GenericBarrier.  Readers use ld.global.cg (L2), so no L1 flush.
-__device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int target, int tid) {
-  named_bar(1, NT);
-  if (tid == 0) {
-    red_release_add(ctr, 1u);
-    while (ld_acquire(ctr) < target) {
-    }
-  }
-  named_bar(1, NT);
-}
-
-__device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
-  return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];
-}
 
 template <bool IMPL, int NV, int TR, int D>
 __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A) {
@@ -199,7 +142,6 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   const int R4 = r >> 2;
   int g[NV];
   bool gv[NV];
-#pragma unroll
   int ge[NV];   // clamped group index: invalid groups read column group 0 and use s = 0
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
@@ -528,6 +470,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       e0 = warp_sum_f64(errsum);
       e1 = warp_sum_f64(brksum);
     }
+    unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
+    if (trc) trc[0] = globaltimer();   // tiles done
     if (A.gpp > 1) {
       // R1: column-major partials part[k * gpp + cta]
 #pragma unroll
@@ -543,7 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         part[(int64_t)(r + 2) * A.gpp + cta] = 0.0;
         part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
       }
-      group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (trc) trc[1] = globaltimer();   // barrier 1 passed
       // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
       for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NW) {
         const double* col = part + (int64_t)k * A.gpp;
@@ -553,7 +498,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         acc = warp_sum_f64(acc);
         if (lane == 0) svec[k] = acc;
       }
-      if (!multi) group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (trc) trc[2] = globaltimer();   // R2 done
+      if (!multi) group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (trc) trc[3] = globaltimer();   // barrier 2 passed
     } else {
       if (tid == 0) {
         S.ext[0] = e0;
@@ -601,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         part[cta] = la;
         part[A.gpp + cta] = lb;
       }
-      group_barrier(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (cta == 0 && tid == 0) {
         la = 0.0;
         lb = 0.0;
