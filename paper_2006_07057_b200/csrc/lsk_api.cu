@@ -473,15 +473,23 @@ static lsk_status feature_map_impl(const lsk_feature_params* p, const float* U, 
   if (!aligned16(Xi)) return fail(LSK_EINVAL, "Xi must be 16-byte aligned");
   char* ws;
   Carve cv;
+  const bool tensor = p->d > 16 && !getenv("LSK_FEATURE_FFMA");   // knob: FFMA A/B only
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
   const size_t oD = cv.take(sizeof(float) * p->r);
+  const size_t oI = tensor ? cv.take(feature_map_tc_image_bytes(p->r, p->d)) : 0;
   LSK_TRY(get_ws(s, cv.off, &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   float* bD = reinterpret_cast<float*>(ws + oD);
-  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, bD, s));
-  LSK_CU(launch_feature_map(X, rows, p->d, U, Wt, b2, bD, p->r, p->eps, Xi, s));
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, tensor ? nullptr : Wt, b2,
+                            bD, s));
+  if (tensor) {
+    LSK_CU(launch_feature_map_tc(X, rows, p->d, U, b2, p->r, p->eps,
+                                 reinterpret_cast<float*>(ws + oI), Xi, s));
+  } else {
+    LSK_CU(launch_feature_map(X, rows, p->d, U, Wt, b2, bD, p->r, p->eps, Xi, s));
+  }
   return LSK_OK;
 }
 

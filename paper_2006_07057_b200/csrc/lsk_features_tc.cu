@@ -1,0 +1,275 @@
+// lsk_features_tc.cu — a3 for large d: the Gaussian positive feature map with
+// the x.u contraction on the 5th-generation tensor cores (tcgen05.mma, kind::tf32, fp32
+// accumulators in TMEM), in 3xTF32 (reading C14: plain TF32 misses the 1e-4 scaling parity):
+//     G = X W^T,  W = (4 log2e / eps) U,  G ~= Xhi Whi^T + Xhi Wlo^T + Xlo Whi^T
+//     xi_ik = 2^( alpha2_i + beta2_k + G_ik ),  alpha2_i = -(2 log2e/eps)|x_i|^2,
+//     beta2_k = log2e (-(2/eps)|u_k|^2 + |u_k|^2/(eps q) + log_scale)
+// hi = cvt.rna.tf32(v), lo = cvt.rna.tf32(v - hi) are formed explicitly, so the MMA sees exactly
+// representable operands.
+//
+// CTA tile 128 rows x 256 anchors, K in chunks of 32 (one 128-byte swizzle row).  Operands
+// live in shared memory in the canonical K-major SWIZZLE_128B layout (8-row x 128 B atoms,
+// SBO = 1024 B): W hi/lo images are pre-built once per call in global memory and brought in
+// with one bulk async copy per chunk (TMA engine, mbarrier complete_tx); X chunks are loaded,
+// split and swizzled by the threads.  One elected thread issues 3 x 4 MMAs (128x256x8) per
+// chunk; tcgen05.commit signals an mbarrier that releases the buffers and, after the last
+// chunk, the epilogue: 8 warps read the accumulator with tcgen05.ld (warp w: TMEM lanes
+// 32(w%4).., columns 128(w/4)..), add alpha2 + beta2, MUFU ex2, store fp32.
+#include <cmath>
+
+#include "lsk_internal.h"
+#include "lsk_ptx.cuh"
+
+namespace lsk {
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 32;
+constexpr int kThreads = 256;
+constexpr int kXBytes = BM * BK * 4;   // 16 KB per hi / lo image
+constexpr int kWBytes = BN * BK * 4;   // 32 KB per hi / lo image
+constexpr double kLog2e = 1.4426950408889634074;
+// smem: xhi | xlo | whi | wlo | beta2[BN] | alpha[BM] | barriers
+constexpr int kOffXhi = 0, kOffXlo = kXBytes, kOffWhi = 2 * kXBytes, kOffWlo = 2 * kXBytes + kWBytes;
+constexpr int kOffBeta = 2 * kXBytes + 2 * kWBytes;
+constexpr int kOffAlpha = kOffBeta + BN * 4;
+constexpr int kOffBar = kOffAlpha + BM * 4;
+constexpr int kSmemBytes = kOffBar + 64 + 1024;   // + alignment slack
+
+// byte offset of element (row, k) inside a K-major SWIZZLE_128B image (rows of 128 B)
+__host__ __device__ __forceinline__ uint32_t swz128(int row, int k) {
+  const uint32_t chunk = (uint32_t)(k >> 2) ^ (uint32_t)(row & 7);
+  return (uint32_t)row * 128u + chunk * 16u + (uint32_t)(k & 3) * 4u;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t y;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+  return __uint_as_float(y);
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, cta_group::1
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// W hi/lo images: [ntile][kchunk][2][BN rows x 128 B swizzled]; rows >= r and k >= d are 0.
+__global__ void w_images_kernel(const float* __restrict__ U, int r, int d, double eps,
+                                float* __restrict__ img) {
+  const int nt = blockIdx.x, kc = blockIdx.y;
+  const int nkc = gridDim.y;
+  char* base = reinterpret_cast<char*>(img) + ((size_t)nt * nkc + kc) * 2 * kWBytes;
+  const double sc = 4.0 * kLog2e / eps;
+  for (int i = threadIdx.x; i < BN * BK; i += blockDim.x) {
+    const int row = i / BK, k = i % BK;
+    const int n = nt * BN + row, c = kc * BK + k;
+    const float w = (n < r && c < d) ? (float)(sc * (double)U[(int64_t)n * d + c]) : 0.f;
+    const float hi = tf32_rna(w);
+    const float lo = tf32_rna(w - hi);
+    *reinterpret_cast<float*>(base + swz128(row, k)) = hi;
+    *reinterpret_cast<float*>(base + kWBytes + swz128(row, k)) = lo;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
+    const float* __restrict__ X, int64_t M, int d, const float* __restrict__ wimg,
+    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* beta_s = reinterpret_cast<float*>(smem + kOffBeta);
+  float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* mbar = wbar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int nkc = (d + BK - 1) / BK;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < BN; i += kThreads) beta_s[i] = (n0 + i < r) ? beta2[n0 + i] : 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  // idesc: D=f32, A=B=tf32, K-major both, N = 256, M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(BM >> 4) << 24);
+
+  // X chunk loader: thread t -> row t/2, k-half t%2 (16 consecutive k)
+  const int xrow = tid >> 1, xk0 = (tid & 1) * 16;
+  const int64_t grow = m0 + xrow;
+  float xx = 0.f;
+
+  for (int kc = 0; kc < nkc; ++kc) {
+    // global loads for this chunk (overlap the previous chunk's MMAs)
+    float v[16];
+    const int cb = kc * BK + xk0;
+    if ((d & 3) == 0 && grow < M && cb + 16 <= d) {   // 16-byte vector loads
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 t4 = __ldg(reinterpret_cast<const float4*>(X + grow * d + cb) + q);
+        v[4 * q] = t4.x; v[4 * q + 1] = t4.y; v[4 * q + 2] = t4.z; v[4 * q + 3] = t4.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = (grow < M && cb + i < d) ? __ldg(X + grow * d + cb + i) : 0.f;
+    }
+    if (kc > 0) mbar_wait(mbar, (uint32_t)((kc - 1) & 1));   // previous MMAs done: buffers free
+    if (tid == 0) {
+      mbar_arrive_expect_tx(wbar, 2 * kWBytes);
+      const char* src = reinterpret_cast<const char*>(wimg) +
+                        ((size_t)blockIdx.y * nkc + kc) * 2 * kWBytes;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              sbase + kOffWhi),
+          "l"(src), "r"(2 * kWBytes), "r"(smem_u32(wbar))
+          : "memory");
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 hi, lo;
+      float* h = &hi.x;
+      float* l = &lo.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = v[q * 4 + e];
+        xx = fmaf(x, x, xx);
+        h[e] = tf32_rna(x);
+        l[e] = tf32_rna(x - h[e]);
+      }
+      const uint32_t off = swz128(xrow, xk0 + q * 4);
+      *reinterpret_cast<float4*>(smem + kOffXhi + off) = hi;
+      *reinterpret_cast<float4*>(smem + kOffXlo + off) = lo;
+    }
+    fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the tensor core
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(wbar, (uint32_t)(kc & 1));
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        const uint64_t axh = umma_desc_sw128(sbase + kOffXhi + kk * 32);
+        const uint64_t axl = umma_desc_sw128(sbase + kOffXlo + kk * 32);
+        const uint64_t bwh = umma_desc_sw128(sbase + kOffWhi + kk * 32);
+        const uint64_t bwl = umma_desc_sw128(sbase + kOffWlo + kk * 32);
+        const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
+        mma_tf32(tmem, axh, bwh, idesc, acc0);
+        mma_tf32(tmem, axh, bwl, idesc, 1u);
+        mma_tf32(tmem, axl, bwh, idesc, 1u);
+      }
+      mma_commit(mbar);
+    }
+  }
+  // alpha2 of each row: the two half-row partials of |x|^2
+  xx += __shfl_xor_sync(0xffffffffu, xx, 1);
+  if ((tid & 1) == 0) alpha_s[xrow] = c2 * xx;
+  mbar_wait(mbar, (uint32_t)((nkc - 1) & 1));
+  tc_fence_after();
+  __syncthreads();
+
+  // epilogue: warp w -> TMEM lanes 32(w%4).., columns 128(w/4) .. +128
+  const int q4 = warp & 3, half = warp >> 2;
+  const int row = q4 * 32 + lane;
+  const int64_t orow = m0 + row;
+  const float al = alpha_s[row];
+#pragma unroll 1
+  for (int cc = 0; cc < 4; ++cc) {
+    const int col = half * 128 + cc * 32;
+    uint32_t a[32];
+    const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)col;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+          "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]),
+          "=r"(a[13]), "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]),
+          "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]),
+          "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]),
+          "=r"(a[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (orow < M) {
+      float* dst = Xi + orow * r + n0 + col;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        if (n0 + col + j < r) {
+          float4 o;
+          o.x = ex2(al + beta_s[col + j + 0] + __uint_as_float(a[j + 0]));
+          o.y = ex2(al + beta_s[col + j + 1] + __uint_as_float(a[j + 1]));
+          o.z = ex2(al + beta_s[col + j + 2] + __uint_as_float(a[j + 2]));
+          o.w = ex2(al + beta_s[col + j + 3] + __uint_as_float(a[j + 3]));
+          st_global_cs(reinterpret_cast<float4*>(dst + j), o);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN)
+                 : "memory");
+  }
+}
+
+}  // namespace tc
+
+size_t feature_map_tc_image_bytes(int r, int d) {
+  const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
+  return (size_t)nt * nkc * 2 * tc::kWBytes;
+}
+
+cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
+                                  const float* beta2, int r, double eps, float* wimg, float* Xi,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
+  tc::w_images_kernel<<<dim3(nt, nkc), 256, 0, s>>>(U, r, d, eps, wimg);
+  count_launch();
+  cudaError_t e = cudaFuncSetAttribute(tc::feature_map_tc_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  const float c2 = (float)(-2.0 * tc::kLog2e / eps);
+  dim3 grid((unsigned)((n + tc::BM - 1) / tc::BM), (unsigned)nt);
+  tc::feature_map_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace lsk

@@ -91,6 +91,11 @@ cudaError_t launch_anchor_prep(const float* U, int r, int d, double eps, double 
 cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
                                const float* Wt, const float* beta2, const float* betaD, int r,
                                double eps, float* Xi, cudaStream_t s);
+// tcgen05 3xTF32 feature map (lsk_features_tc.cu), used for d > 16
+size_t feature_map_tc_image_bytes(int r, int d);
+cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
+                                  const float* beta2, int r, double eps, float* wimg, float* Xi,
+                                  cudaStream_t s);
 cudaError_t launch_rot_value(const float* u, const float* v, const float* a, const float* b,
                              int64_t n, int64_t m, int batch, double* partials, double* out2,
                              cudaStream_t s);
