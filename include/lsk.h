@@ -120,7 +120,8 @@ lsk_status lsk_philox_words(uint64_t seed, int32_t r, int32_t d, uint32_t* out, 
 /* ---- a3: feature map xi = phi_theta(X) --------------------- */
 /* Xi (n x r, fp32, device): Xi[i][k] = exp(-(2/eps)|x_i - U_k|^2 + |U_k|^2/(eps q)
  *   + log_scale).  d <= 16: direct difference form on FFMA; d > 16: expanded form
- * |x|^2 + |U|^2 - 2 x.U with the contraction tiled through shared memory. r % 4 == 0. */
+ * |x|^2 + |U|^2 - 2 x.U with the x.U contraction on the tcgen05 tensor cores in 3xTF32
+ * (TMEM accumulators, exp epilogue).  r % 4 == 0. */
 lsk_status lsk_feature_map(const lsk_feature_params* p, const float* U, const float* X,
                            int64_t n, float* Xi, void* stream);
 /* Batched: X is (batch, n, d), Xi is (batch, n, r); one shared anchor draw (config 4). */
@@ -165,6 +166,22 @@ lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const f
 lsk_status lsk_rot_value_batched(const float* u, const float* v, const float* a,
                                  const float* b, int64_t n, int64_t m, int32_t batch,
                                  double eps, double* rots_host, void* stream);
+
+/* ---- NEXT f1: Sinkhorn divergence (eq. reg-sdiv) ------------------- */
+/* W_bar(mu,nu) = W(mu,nu) - (W(mu,mu) + W(nu,nu)) / 2, each W the dual estimate of Alg. 1
+ * on K_theta with ONE anchor draw shared by the three problems (a single cost c_theta).
+ * Three persistent solves with the options o (fixed T or tolerance); out4_host (host, 4
+ * doubles) = {W_bar, W_xy, W_xx, W_yy}; reps3 (host, 3 reports, nullable) in the same order
+ * (xy, xx, yy).  Scalings are not returned (scratch in the workspace).  Synchronises. */
+lsk_status lsk_sinkhorn_divergence(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                   int32_t r, const float* a, const float* b, double eps,
+                                   const lsk_solve_opts* o, double* out4_host,
+                                   lsk_report* reps3, void* stream);
+lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const float* U,
+                                            const float* X, int64_t n, const float* Y,
+                                            int64_t m, const float* a, const float* b,
+                                            const lsk_solve_opts* o, double* out4_host,
+                                            lsk_report* reps3, void* stream);
 
 /* ---- whole path with HOST buffers (end-to-end entry point) ---------------------------- */
 /* X_host (n x d), Y_host (m x d), a_host, b_host (host memory, pinned or pageable).  Copies

@@ -293,3 +293,29 @@ def rot(X, Y, a, b, eps: float, r: int, seed: int, T: Optional[int] = None,
     sol.update(rot=dual_estimate(sol["u"], sol["v"], a, b, eps), U=U, xi=xi, zeta=zeta,
                params=prm)
     return sol
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT row f1: Sinkhorn divergence (eq. reg-sdiv)
+# ---------------------------------------------------------------------------------------
+def sinkhorn_divergence(X, Y, a, b, eps: float, r: int, seed: int, T: Optional[int] = None,
+                        tol: Optional[float] = None, R: Optional[float] = None) -> dict:
+    """W_bar(mu,nu) = W(mu,nu) - (W(mu,mu) + W(nu,nu)) / 2, each W the dual
+    estimate of Alg. 1 on K_theta with ONE anchor draw theta shared by the three problems
+    (c_theta is a single cost, eq. cost).  R defaults to the max norm over both
+    clouds, so the three solves use the same (q, sigma, theta)."""
+    if R is None:
+        R = max_norm(X, Y)
+    d = np.asarray(X).shape[1]
+    prm = gaussian_params(eps, d, r, R)
+    U = draw_anchors(r, d, prm["sigma"], seed)
+    xi = feature_matrix(X, U, eps, prm["q"])
+    zeta = feature_matrix(Y, U, eps, prm["q"])
+    out = {}
+    for name, (F, G, wa, wb) in {"xy": (xi, zeta, a, b), "xx": (xi, xi, a, a),
+                                  "yy": (zeta, zeta, b, b)}.items():
+        s = sinkhorn_factored(F, G, wa, wb, T=T, tol=tol)
+        out[name] = dual_estimate(s["u"], s["v"], wa, wb, eps)
+    out["div"] = out["xy"] - 0.5 * (out["xx"] + out["yy"])
+    out.update(R=R, U=U)
+    return out

@@ -86,6 +86,13 @@ _SIGS = {
                               P(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]),
     "lsk_rot_value_batched": (c_i32, [c_f32p, c_f32p, c_f32p, c_f32p, c_i64, c_i64, c_i32,
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_sinkhorn_divergence": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
+                                        ctypes.c_double, P(lsk_solve_opts), ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_sinkhorn_divergence_implicit": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64,
+                                                 c_f32p, c_i64, c_f32p, c_f32p,
+                                                 P(lsk_solve_opts), ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_void_p]),
     "lsk_rot_host": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
                              ctypes.c_double, c_i32, ctypes.c_uint64, ctypes.c_double,
                              P(lsk_solve_opts), c_i32, c_f32p, c_f32p, P(lsk_report)]),
@@ -96,6 +103,9 @@ _SIGS = {
 }
 EXPORTED = sorted(_SIGS)
 for _name, (_res, _args) in _SIGS.items():
+    if not hasattr(_lib, _name):
+        raise ImportError("liblsk.so is stale (missing %s): rebuild with "
+                          "`python paper_2006_07057_b200/build.py`" % _name)
     _fn = getattr(_lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args
@@ -260,6 +270,51 @@ def lsk_rot_value_batched(u, v, a, b, eps, stream=None):
     _check(_lib.lsk_rot_value_batched(_f32(u), _f32(v), _f32(a), _f32(b), n, m, B, float(eps),
                                       out, _stream(stream)), "lsk_rot_value_batched")
     return list(out)
+
+
+def _div_result(out, reps):
+    return dict(div=out[0], xy=out[1], xx=out[2], yy=out[3],
+                reports=[rp.as_dict() for rp in reps])
+
+
+def lsk_sinkhorn_divergence(Xi, Zeta, a, b, eps, opts, stream=None):
+    """W_bar(mu,nu) = W(mu,nu) - (W(mu,mu) + W(nu,nu))/2 on device factors."""
+    out = (ctypes.c_double * 4)()
+    reps = (lsk_report * 3)()
+    _check(_lib.lsk_sinkhorn_divergence(_f32(Xi), Xi.shape[0], _f32(Zeta), Zeta.shape[0],
+                                        Xi.shape[1], _f32(a), _f32(b), float(eps),
+                                        ctypes.byref(opts), out, reps, _stream(stream)),
+           "lsk_sinkhorn_divergence")
+    return _div_result(out, reps)
+
+
+def lsk_sinkhorn_divergence_implicit(p, U, X, Y, a, b, opts, stream=None):
+    out = (ctypes.c_double * 4)()
+    reps = (lsk_report * 3)()
+    _check(_lib.lsk_sinkhorn_divergence_implicit(ctypes.byref(p), _f32(U), _f32(X), X.shape[0],
+                                                 _f32(Y), Y.shape[0], _f32(a), _f32(b),
+                                                 ctypes.byref(opts), out, reps,
+                                                 _stream(stream)),
+           "lsk_sinkhorn_divergence_implicit")
+    return _div_result(out, reps)
+
+
+def sinkhorn_divergence(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0,
+                        variant="stream", max_iters=None, stream=None):
+    """Whole divergence path on device tensors: shared params/anchors, features, 3 solves."""
+    import torch
+    d = X.shape[1]
+    p = lsk_feature_params_init(eps, d, r, R, seed, X, Y, stream=stream)
+    U = torch.empty((r, d), dtype=torch.float32, device=X.device)
+    lsk_draw_anchors(p, U, stream)
+    opts = make_opts(iters if iters is not None else (max_iters or 1000), tol)
+    if variant == "implicit":
+        return lsk_sinkhorn_divergence_implicit(p, U, X, Y, a, b, opts, stream)
+    Xi = torch.empty((X.shape[0], r), dtype=torch.float32, device=X.device)
+    Ze = torch.empty((Y.shape[0], r), dtype=torch.float32, device=X.device)
+    lsk_feature_map(p, U, X, Xi, stream)
+    lsk_feature_map(p, U, Y, Ze, stream)
+    return lsk_sinkhorn_divergence(Xi, Ze, a, b, eps, opts, stream)
 
 
 def lsk_rot_host(X, Y, a, b, eps, r, seed, opts, R=0.0, variant=0, u_out=None, v_out=None):

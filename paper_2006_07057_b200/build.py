@@ -1,4 +1,5 @@
-"""Build liblsk.so (sm_100a) in-tree with nvcc.  Usage: python -m paper_2006_07057_b200.build"""
+"""Build liblsk.so (sm_100a) in-tree with nvcc.  Usage: python paper_2006_07057_b200/build.py [-v]
+(a script on purpose: importing the package would load a possibly stale liblsk.so)."""
 from __future__ import annotations
 
 import concurrent.futures

@@ -621,6 +621,43 @@ lsk_status lsk_rot_value_batched(const float* u, const float* v, const float* a,
   return LSK_OK;
 }
 
+// ---------------------------------------------------------------- Sinkhorn divergence --
+static lsk_status divergence_impl(bool impl, const float* F, int64_t n, const float* G,
+                                  int64_t m, int r, int d, const float* a, const float* b,
+                                  double eps, const float* Wt, const float* b2, float c2,
+                                  const lsk_solve_opts* o, double* out4, lsk_report* reps3,
+                                  cudaStream_t s, char* ws, Carve& cv) {
+  const int64_t mx = std::max(n, m);
+  float* us = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * mx));
+  float* vs = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * mx));
+  struct Prob { const float *f0, *f1, *w0, *w1; int64_t r0, r1; } probs[3] = {
+      {F, G, a, b, n, m}, {F, F, a, a, n, n}, {G, G, b, b, m, m}};
+  double W[3];
+  lsk_status worst = LSK_OK;
+  for (int k = 0; k < 3; ++k) {
+    SinkArgs A{};
+    if (impl) { A.X[0] = probs[k].f0; A.X[1] = probs[k].f1; }
+    else { A.F[0] = probs[k].f0; A.F[1] = probs[k].f1; }
+    A.rows[0] = probs[k].r0; A.rows[1] = probs[k].r1;
+    A.w[0] = probs[k].w0; A.w[1] = probs[k].w1;
+    A.out[0] = us; A.out[1] = vs;
+    A.r = r; A.d = d; A.eps = eps;
+    A.Wt = Wt; A.beta2 = b2; A.c2 = c2;
+    Carve cv2 = cv;   // each solve reuses the same workspace tail
+    lsk_report rep{};
+    lsk_status st = run_solve(A, impl, 1, o, &rep, nullptr, s, ws, cv2);
+    if (st < 0) return st;
+    if (st > worst) worst = st;
+    W[k] = rep.rot;
+    if (reps3) reps3[k] = rep;
+  }
+  out4[0] = W[0] - 0.5 * (W[1] + W[2]);
+  out4[1] = W[0];
+  out4[2] = W[1];
+  out4[3] = W[2];
+  return worst;
+}
+
 // ---------------------------------------------------------------- host-buffer pipeline --
 lsk_status lsk_rot_host(const float* X_host, int64_t n, const float* Y_host, int64_t m,
                         int32_t d, const float* a_host, const float* b_host, double eps,
@@ -688,6 +725,46 @@ lsk_status lsk_rot_host(const float* X_host, int64_t n, const float* Y_host, int
   LSK_CU(cudaStreamSynchronize(s));
   if (rep) *rep = local;
   return st;
+}
+
+lsk_status lsk_sinkhorn_divergence(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                   int32_t r, const float* a, const float* b, double eps,
+                                   const lsk_solve_opts* o, double* out4_host,
+                                   lsk_report* reps3, void* stream) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (!Xi || !Zeta || !a || !b || !out4_host) return fail(LSK_EINVAL, "NULL argument");
+  if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t mx = std::max(n, m);
+  char* ws;
+  LSK_TRY(get_ws(s, 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(r, mx, 1, 2 * num_sms()), &ws));
+  Carve cv;
+  return divergence_impl(false, Xi, n, Zeta, m, r, 1, a, b, eps, nullptr, nullptr, 0.f, o,
+                         out4_host, reps3, s, ws, cv);
+}
+
+lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const float* U,
+                                            const float* X, int64_t n, const float* Y,
+                                            int64_t m, const float* a, const float* b,
+                                            const lsk_solve_opts* o, double* out4_host,
+                                            lsk_report* reps3, void* stream) {
+  if (!p) return fail(LSK_EINVAL, "params NULL");
+  LSK_TRY(check_common(n, m, p->r, p->eps));
+  if (!U || !X || !Y || !a || !b || !out4_host) return fail(LSK_EINVAL, "NULL argument");
+  if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t mx = std::max(n, m);
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off + 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(p->r, mx, 1, 2 * num_sms()), &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  return divergence_impl(true, X, n, Y, m, p->r, p->d, a, b, p->eps, Wt, b2,
+                         (float)(-2.0 * 1.4426950408889634074 / p->eps), o, out4_host, reps3, s,
+                         ws, cv);
 }
 
 // ---------------------------------------------------------------- NCCL communicator -----

@@ -16,6 +16,7 @@
 // boundary, stopping test and the fp64 read-out are those of the streaming kernel.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "lsk_internal.h"
 #include "lsk_ptx.cuh"
@@ -462,7 +463,10 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 // r <= 4096 -> (512, 1, 2, 2).  Always 512 threads, one CTA per SM.
 void implicit_config(int r, int* nt, int* nv, int* tr) {
   const int r4 = (r + 3) / 4;
-  if (r4 <= 256) { *nt = 256; *nv = 1; *tr = 8; }
+  if (r4 <= 256) {
+    *nt = 256; *nv = 1; *tr = 8;
+    if (const char* e = getenv("LSK_ITR")) *tr = atoi(e) == 16 ? 16 : 8;   // tuning knob
+  }
   else if (r4 <= 512) { *nt = 512; *nv = 1; *tr = 8; }
   else { *nt = 512; *nv = 2; *tr = 2; }
 }
@@ -470,7 +474,7 @@ void implicit_config(int r, int* nt, int* nv, int* tr) {
 #define LSK_IMPL2(X, TS, TM, NV, TR) X(TS, TM, NV, TR, 1) X(TS, TM, NV, TR, 2) \
   X(TS, TM, NV, TR, 3) X(TS, TM, NV, TR, 4) X(TS, TM, NV, TR, 5) X(TS, TM, NV, TR, 6)     \
   X(TS, TM, NV, TR, 7) X(TS, TM, NV, TR, 8)
-#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 512, 1, 1, 8) \
+#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 256, 2, 1, 16) LSK_IMPL2(X, 512, 1, 1, 8) \
   LSK_IMPL2(X, 512, 1, 2, 2)
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {

@@ -332,3 +332,26 @@ def test_smoke_entry_point(L):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     ge = importlib.import_module("__graft_entry__")
     ge.smoke()
+
+
+# ------------------------------------------------------------------ NEXT f1: divergence ----
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
+def test_sinkhorn_divergence(L, variant):
+    """W_bar(mu,nu) = W(mu,nu) - (W(mu,mu) + W(nu,nu))/2 vs the oracle; each W to
+    1e-5 relative; W_bar (a difference) to 1e-5 of the sum of magnitudes; W_bar(mu,mu) = 0
+    exactly (the three solves are the same computation)."""
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=3001, m=2503)
+    T = 200
+    ref = O.sinkhorn_divergence(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r,
+                                cfg.anchor_seed, T=T)
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    got = L.sinkhorn_divergence(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T,
+                                variant=variant)
+    for k in ("xy", "xx", "yy"):
+        assert abs(got[k] - ref[k]) <= ROT_TOL * abs(ref[k]), (k, got[k], ref[k])
+    scale = abs(ref["xy"]) + abs(ref["xx"]) + abs(ref["yy"])
+    assert abs(got["div"] - ref["div"]) <= ROT_TOL * scale, (got["div"], ref["div"])
+    same = L.sinkhorn_divergence(X, X, a, a, cfg.eps, cfg.r, cfg.anchor_seed, iters=50,
+                                 variant=variant)
+    assert same["div"] == 0.0
