@@ -183,6 +183,20 @@ lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const f
                                             const lsk_solve_opts* o, double* out4_host,
                                             lsk_report* reps3, void* stream);
 
+/* ---- NEXT f2: envelope gradients (Prop. diff-gene + chain rule) ------ */
+/* At the scalings (u, v) of a solve (streaming factors Xi, Zeta of X, Y under anchors U and
+ * params p), with theta = U and q fixed: dW/dK = -eps u v^T gives
+ *   gX_i = 4 u_i sum_k Xi_ik s_u,k (x_i - U_k),   s_u = Zeta^T v,
+ *   gY_j = 4 v_j sum_k Zeta_jk s_v,k (y_j - U_k), s_v = Xi^T u,
+ *   gU_k = -4 (s_u,k B_x,k + s_v,k B_y,k) - (4/q) s_u,k s_v,k U_k,
+ *          B_x,k = sum_i u_i Xi_ik (x_i - U_k), B_y,k likewise.
+ * gX (n x d), gY (m x d), gU (r x d): device fp32, each nullable.  d <= 16 (LSK_EDIM
+ * otherwise).  Row sums are fp64 with fixed-order partials.  Asynchronous. */
+lsk_status lsk_rot_gradient(const lsk_feature_params* p, const float* U, const float* X,
+                            int64_t n, const float* Y, int64_t m, const float* Xi,
+                            const float* Zeta, const float* u, const float* v, float* gX,
+                            float* gY, float* gU, void* stream);
+
 /* ---- whole path with HOST buffers (end-to-end entry point) ---------------------------- */
 /* X_host (n x d), Y_host (m x d), a_host, b_host (host memory, pinned or pageable).  Copies
  * inputs to the device, runs a1-a9 (variant 0 = auto, 1 = streaming, 2 = implicit), copies

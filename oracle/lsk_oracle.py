@@ -319,3 +319,29 @@ def sinkhorn_divergence(X, Y, a, b, eps: float, r: int, seed: int, T: Optional[i
     out["div"] = out["xy"] - 0.5 * (out["xx"] + out["yy"])
     out.update(R=R, U=U)
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT row f2: envelope gradients (Prop. diff-gene, chain rule PAPER.md:414-420)
+# ---------------------------------------------------------------------------------------
+def envelope_gradients(X, Y, U, xi, zeta, u, v, eps: float, q: float) -> dict:
+    """Gradients of W_{eps,c_theta} at the optimal scalings (u, v), with the anchors theta = U
+    and q held fixed.  Prop. diff-gene: dW/dK = -eps u v^T; with K = xi^T zeta (paper layout,
+    xi r x n) this gives dW/dxi = -eps (zeta v) u^T and dW/dzeta = -eps (xi u) v^T
+    (PAPER.md:414-420).  For the Gaussian map,
+      d xi_ki / d x_i = -(4/eps) (x_i - u_k) xi_ki,
+      d xi_ki / d u_k = xi_ki ( (4/eps)(x_i - u_k) + 2 u_k / (eps q) ),
+    and the same for zeta with y_j.  Returns gX (n,d), gY (m,d), gU (r,d)."""
+    X = np.asarray(X, np.float64)
+    Y = np.asarray(Y, np.float64)
+    U = np.asarray(U, np.float64)
+    dW_dxi = -eps * np.outer(zeta @ v, u)           # r x n
+    dW_dzeta = -eps * np.outer(xi @ u, v)           # r x m
+    diffx = X[None, :, :] - U[:, None, :]           # r x n x d  (x_i - u_k)
+    diffy = Y[None, :, :] - U[:, None, :]
+    gX = np.einsum("ki,kid->id", dW_dxi * xi, -(4.0 / eps) * diffx)
+    gY = np.einsum("kj,kjd->jd", dW_dzeta * zeta, -(4.0 / eps) * diffy)
+    gU = (np.einsum("ki,kid->kd", dW_dxi * xi, (4.0 / eps) * diffx)
+          + np.einsum("kj,kjd->kd", dW_dzeta * zeta, (4.0 / eps) * diffy)
+          + ((dW_dxi * xi).sum(1) + (dW_dzeta * zeta).sum(1))[:, None] * 2.0 * U / (eps * q))
+    return dict(gX=gX, gY=gY, gU=gU)

@@ -93,6 +93,9 @@ _SIGS = {
                                                  c_f32p, c_i64, c_f32p, c_f32p,
                                                  P(lsk_solve_opts), ctypes.c_void_p,
                                                  ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_rot_gradient": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p, c_i64,
+                                 c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p,
+                                 ctypes.c_void_p]),
     "lsk_rot_host": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
                              ctypes.c_double, c_i32, ctypes.c_uint64, ctypes.c_double,
                              P(lsk_solve_opts), c_i32, c_f32p, c_f32p, P(lsk_report)]),
@@ -315,6 +318,22 @@ def sinkhorn_divergence(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0,
     lsk_feature_map(p, U, X, Xi, stream)
     lsk_feature_map(p, U, Y, Ze, stream)
     return lsk_sinkhorn_divergence(Xi, Ze, a, b, eps, opts, stream)
+
+
+def lsk_rot_gradient(p, U, X, Y, Xi, Zeta, u, v, want=("X", "Y", "U"), stream=None):
+    """Envelope gradients dW/dX, dW/dY, dW/dU at the scalings (u, v)."""
+    import torch
+    d, r = X.shape[1], U.shape[0]
+    out = {k: torch.empty(shp, dtype=torch.float32, device=X.device)
+           for k, shp in (("X", (X.shape[0], d)), ("Y", (Y.shape[0], d)), ("U", (r, d)))
+           if k in want}
+    _check(_lib.lsk_rot_gradient(ctypes.byref(p), _f32(U), _f32(X), X.shape[0], _f32(Y),
+                                 Y.shape[0], _f32(Xi), _f32(Zeta), _f32(u), _f32(v),
+                                 _f32(out["X"]) if "X" in out else None,
+                                 _f32(out["Y"]) if "Y" in out else None,
+                                 _f32(out["U"]) if "U" in out else None, _stream(stream)),
+           "lsk_rot_gradient")
+    return out
 
 
 def lsk_rot_host(X, Y, a, b, eps, r, seed, opts, R=0.0, variant=0, u_out=None, v_out=None):

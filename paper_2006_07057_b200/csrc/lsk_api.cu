@@ -767,6 +767,21 @@ lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const f
                          ws, cv);
 }
 
+lsk_status lsk_rot_gradient(const lsk_feature_params* p, const float* U, const float* X,
+                            int64_t n, const float* Y, int64_t m, const float* Xi,
+                            const float* Zeta, const float* u, const float* v, float* gX,
+                            float* gY, float* gU, void* stream) {
+  if (!p || !U || !X || !Y || !Xi || !Zeta || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  LSK_TRY(check_common(n, m, p->r, p->eps));
+  if (p->d > 16) return fail(LSK_EDIM, "gradients support d <= 16");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  LSK_TRY(get_ws(s, grad_workspace_bytes(p->r, p->d), &ws));
+  LSK_CU(launch_gradients(X, n, Y, m, p->d, U, p->r, p->q, Xi, Zeta, u, v, gX, gY, gU,
+                          reinterpret_cast<double*>(ws), s));
+  return LSK_OK;
+}
+
 // ---------------------------------------------------------------- NCCL communicator -----
 lsk_status lsk_comm_get_unique_id(void* out_host) {
   if (!out_host) return fail(LSK_EINVAL, "out is NULL");

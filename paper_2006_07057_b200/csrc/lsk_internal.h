@@ -96,6 +96,12 @@ size_t feature_map_tc_image_bytes(int r, int d);
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
                                   const float* beta2, int r, double eps, float* wimg, float* Xi,
                                   cudaStream_t s);
+// envelope gradients (lsk_grad.cu)
+size_t grad_workspace_bytes(int r, int d);
+cudaError_t launch_gradients(const float* X, int64_t n, const float* Y, int64_t m, int d,
+                             const float* U, int r, double q, const float* Xi, const float* Zeta,
+                             const float* u, const float* v, float* gX, float* gY, float* gU,
+                             double* ws, cudaStream_t s);
 cudaError_t launch_rot_value(const float* u, const float* v, const float* a, const float* b,
                              int64_t n, int64_t m, int batch, double* partials, double* out2,
                              cudaStream_t s);

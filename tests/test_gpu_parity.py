@@ -355,3 +355,26 @@ def test_sinkhorn_divergence(L, variant):
     same = L.sinkhorn_divergence(X, X, a, a, cfg.eps, cfg.r, cfg.anchor_seed, iters=50,
                                  variant=variant)
     assert same["div"] == 0.0
+
+
+# ------------------------------------------------------------------ NEXT f2: gradients -----
+@pytest.mark.parametrize("cfg_key,n,m", [(1, 500, 500), (2, 2049, 1531), (5, 3001, 2999)])
+def test_envelope_gradients(L, cfg_key, n, m):
+    """dW/dX, dW/dY, dW/dU from the GPU solve vs the oracle's chain rule
+    (itself pinned by finite differences) on the oracle's own scalings after the same T;
+    max abs error <= 2e-4 of the largest gradient entry (sums with sign cancellation)."""
+    cfg = synth.get_config(cfg_key)
+    prob = synth.make_problem(cfg, n=n, m=m)
+    T = 100
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
+    gref = O.envelope_gradients(prob["X"], prob["Y"], ref["U"], ref["xi"], ref["zeta"], ref["u"],
+                                ref["v"], cfg.eps, ref["params"]["q"])
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    res = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T)
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, cfg.r, 0.0, cfg.anchor_seed, X, Y)
+    g = L.lsk_rot_gradient(p, res["U"], X, Y, res["Xi"], res["Zeta"], res["u"], res["v"])
+    for k, key in (("X", "gX"), ("Y", "gY"), ("U", "gU")):
+        got = g[k].cpu().double().numpy()
+        want = gref[key]
+        err = np.abs(got - want).max() / np.abs(want).max()
+        assert err <= 2e-4, (k, err)

@@ -214,3 +214,33 @@ def test_divergence_pins():
     # the Gram kernel k_theta = phi^T phi is positive semi-definite: W_bar >= 0 (Feydy et al.
     # 2019, Thm 1) — checked as a sanity property on these inputs only
     assert d1["div"] > -1e-10
+
+
+# ---------------- NEXT f2: envelope gradients, pinned by finite differences ---------------------
+def test_envelope_gradients_finite_differences():
+    """dW/dx_i, dW/dy_j, dW/du_k from Prop. diff-gene + chain rule vs
+    central finite differences of W_hat at tight convergence, theta = U and R (so q) fixed."""
+    prob = synth.random_small(31, 14, 11, 2)
+    X, Y = prob["X"].astype(np.float64), prob["Y"].astype(np.float64)
+    a = prob["a"].astype(np.float64); a /= a.sum()
+    b = prob["b"].astype(np.float64); b /= b.sum()
+    eps, r, R = 0.6, 24, 2.0
+    prm = O.gaussian_params(eps, 2, r, R)
+    U = O.draw_anchors(r, 2, prm["sigma"], 4)
+
+    def W(X_, Y_, U_):
+        return O.rot(X_, Y_, a, b, eps, r, 0, tol=1e-14, R=R, U=U_)["rot"]
+
+    res = O.rot(X, Y, a, b, eps, r, 0, tol=1e-14, R=R, U=U)
+    g = O.envelope_gradients(X, Y, U, res["xi"], res["zeta"], res["u"], res["v"], eps, prm["q"])
+    h = 1e-5
+    for name, arr, grad in (("X", X, g["gX"]), ("Y", Y, g["gY"]), ("U", U, g["gU"])):
+        for (i, c) in [(0, 0), (3, 1), (arr.shape[0] - 1, 0)]:
+            P, M = arr.copy(), arr.copy()
+            P[i, c] += h
+            M[i, c] -= h
+            args_p = dict(X=X, Y=Y, U=U)
+            args_m = dict(X=X, Y=Y, U=U)
+            args_p[name], args_m[name] = P, M
+            fd = (W(args_p["X"], args_p["Y"], args_p["U"]) - W(args_m["X"], args_m["Y"], args_m["U"])) / (2 * h)
+            assert abs(fd - grad[i, c]) <= 1e-6 * max(1.0, abs(fd)), (name, i, c, fd, grad[i, c])
