@@ -129,6 +129,19 @@ lsk_status lsk_feature_map_batched(const lsk_feature_params* p, const float* U,
                                    const float* X, int64_t n, int32_t batch, float* Xi,
                                    void* stream);
 
+/* NEXT f3: perturbed arc-cosine positive features (Lemma decomp-arccos, PAPER.md:947-989;
+ * main text PAPER.md:377-382).  Anchors u_k ~ N(0, sigma^2 I) with sigma = p->sigma > 1
+ * (draw them with lsk_draw_anchors on the same p); s_degree in {0,1,2}; kappa > 0.
+ * Xi is n x (r+4): Xi[i][k] = sigma^{d/2} sqrt(2) max(0, u_k.x_i)^s
+ * exp(-|u_k|^2 (1 - 1/sigma^2)/4) / sqrt(r) for k < r, Xi[i][r] = sqrt(kappa), and
+ * Xi[i][r+1..r+3] = 0 — the r kappa slots of phi_theta collapse into one column (same
+ * k_theta), padded to a multiple of 4.  Pass r+4 as the rank to the Sinkhorn calls.  Unbiased
+ * for k_s + kappa with the main-text k_s (reading C21).  d <= 16: FFMA; d > 16: tcgen05
+ * 3xTF32 contraction with a relu^s epilogue. */
+lsk_status lsk_feature_map_arccos(const lsk_feature_params* p, int32_t s_degree, double kappa,
+                                  const float* U, const float* X, int64_t n, float* Xi,
+                                  void* stream);
+
 /* ---- a4-a9: Alg. 1 on K_theta = Xi Zeta^T, streaming the factors from HBM ---------- */
 /* One persistent launch runs every iteration: per iteration a zeta-pass
  * (t_j = zeta_j . s_v, v_j = b_j / t_j, s_u += v_j zeta_j) and a xi-pass (mirror), each

@@ -8,4 +8,5 @@ from .lsk_oracle import (lambert_w0, max_norm, gaussian_params, philox4x32_10, p
                          standard_normals, draw_anchors, gaussian_phi, feature_matrix,
                          feature_entries_scaled, sinkhorn, sinkhorn_factored, sinkhorn_dense,
                          dual_estimate, primal_objective, gaussian_kernel_dense,
-                         marginal_error, rot, sinkhorn_divergence, envelope_gradients)
+                         marginal_error, rot, sinkhorn_divergence, envelope_gradients,
+                         arccos_phi, arccos_kernel, feature_matrix_arccos)

@@ -345,3 +345,48 @@ def envelope_gradients(X, Y, U, xi, zeta, u, v, eps: float, q: float) -> dict:
           + np.einsum("kj,kjd->kd", dW_dzeta * zeta, (4.0 / eps) * diffy)
           + ((dW_dxi * xi).sum(1) + (dW_dzeta * zeta).sum(1))[:, None] * 2.0 * U / (eps * q))
     return dict(gX=gX, gY=gY, gU=gU)
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT row f3: perturbed arc-cosine positive features (Lemma decomp-arccos, PAPER.md:947-989;
+# main text PAPER.md:377-382).  Reading C21: k_s uses the main-text Theta_s = sqrt(2) max(0,.)^s
+# (PAPER.md:379), i.e. Cho & Saul's k_s = (1/pi)|x|^s|y|^s J_s(angle); the appendix proof drops
+# the factor 2 of sqrt(2)^2 — the map as stated is unbiased for k_s + kappa with this k_s.
+# ---------------------------------------------------------------------------------------
+def arccos_phi(x, u, sigma: float, s: int, kappa: float) -> np.ndarray:
+    """phi(x,u) = (sigma^{d/2} sqrt(2) max(0,u^T x)^s exp(-|u|^2/4 (1 - 1/sigma^2)), sqrt(kappa))
+    (PAPER.md:951-953).  Returns (..., 2)."""
+    x = np.asarray(x, np.float64)
+    u = np.asarray(u, np.float64)
+    d = x.shape[-1]
+    ux = (x * u).sum(-1)
+    relu = np.maximum(0.0, ux)
+    pw = np.where(ux > 0, 1.0, 0.0) if s == 0 else relu ** s
+    first = sigma ** (d / 2.0) * math.sqrt(2.0) * pw * np.exp(-(u * u).sum(-1) / 4.0 * (1.0 - 1.0 / sigma ** 2))
+    return np.stack([first, np.full_like(first, math.sqrt(kappa))], axis=-1)
+
+
+def arccos_kernel(x, y, s: int) -> float:
+    """k_s(x,y) = (1/pi)|x|^s|y|^s J_s(theta) (Cho & Saul 2009, the kernel of PAPER.md:379):
+    J_0 = pi - theta, J_1 = sin + (pi - theta) cos, J_2 = 3 sin cos + (pi - theta)(1 + 2 cos^2)."""
+    x = np.asarray(x, np.float64)
+    y = np.asarray(y, np.float64)
+    nx, ny = np.linalg.norm(x), np.linalg.norm(y)
+    c = float(np.clip(x @ y / (nx * ny), -1.0, 1.0))
+    th = math.acos(c)
+    sn = math.sin(th)
+    J = {0: math.pi - th, 1: sn + (math.pi - th) * c,
+         2: 3.0 * sn * c + (math.pi - th) * (1.0 + 2.0 * c * c)}[s]
+    return (nx ** s) * (ny ** s) * J / math.pi
+
+
+def feature_matrix_arccos(X, U, sigma: float, s: int, kappa: float) -> np.ndarray:
+    """xi for the arc-cosine map in the paper layout with the kappa slot collapsed: rows
+    0..r-1 = phi_1(x_i, u_k)/sqrt(r), row r = sqrt(kappa) (the r identical kappa slots of
+    phi_theta(x) = r^{-1/2}(phi(x,u_1),...,phi(x,u_r)) contribute exactly kappa to every
+    k_theta(x,y), as one column sqrt(kappa) does).  Shape (r+1, n)."""
+    X = np.asarray(X, np.float64)
+    U = np.asarray(U, np.float64)
+    r = U.shape[0]
+    ph = arccos_phi(X[None, :, :], U[:, None, :], sigma, s, kappa)[..., 0] / math.sqrt(r)
+    return np.vstack([ph, np.full((1, X.shape[0]), math.sqrt(kappa))])

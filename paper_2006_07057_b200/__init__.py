@@ -70,6 +70,8 @@ _SIGS = {
                                 ctypes.c_void_p]),
     "lsk_feature_map_batched": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_i32,
                                         c_f32p, ctypes.c_void_p]),
+    "lsk_feature_map_arccos": (c_i32, [P(lsk_feature_params), c_i32, ctypes.c_double, c_f32p,
+                                       c_f32p, c_i64, c_f32p, ctypes.c_void_p]),
     "lsk_factored_sinkhorn": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
                                       ctypes.c_double, P(lsk_solve_opts), c_f32p, c_f32p,
                                       P(lsk_report), ctypes.c_void_p, ctypes.c_void_p]),
@@ -214,6 +216,20 @@ def lsk_feature_map(p: lsk_feature_params, U, X, Xi, stream=None):
     _check(_lib.lsk_feature_map(ctypes.byref(p), _f32(U), _f32(X), X.shape[0], _f32(Xi),
                                 _stream(stream)), "lsk_feature_map")
     return Xi
+
+
+def lsk_feature_map_arccos(p, s_degree, kappa, U, X, Xi, stream=None):
+    """Arc-cosine features into Xi (n x (r+4)); see include/lsk.h."""
+    _check(_lib.lsk_feature_map_arccos(ctypes.byref(p), int(s_degree), float(kappa), _f32(U),
+                                       _f32(X), X.shape[0], _f32(Xi), _stream(stream)),
+           "lsk_feature_map_arccos")
+    return Xi
+
+
+def arccos_params(d, r, sigma, seed, eps):
+    """lsk_feature_params for the arc-cosine map: only d, r, sigma, seed (anchors) and eps
+    (the Sinkhorn temperature) are used."""
+    return lsk_feature_params(float(eps), 0.0, 0.0, float(sigma), 0.0, int(d), int(r), int(seed))
 
 
 def lsk_feature_map_batched(p: lsk_feature_params, U, X, Xi, stream=None):

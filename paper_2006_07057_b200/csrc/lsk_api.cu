@@ -498,6 +498,35 @@ lsk_status lsk_feature_map(const lsk_feature_params* p, const float* U, const fl
   return feature_map_impl(p, U, X, n, Xi, static_cast<cudaStream_t>(stream));
 }
 
+lsk_status lsk_feature_map_arccos(const lsk_feature_params* p, int32_t s_degree, double kappa,
+                                  const float* U, const float* X, int64_t n, float* Xi,
+                                  void* stream) {
+  if (!p || !U || !X || !Xi) return fail(LSK_EINVAL, "NULL argument");
+  if (p->r < 4 || p->r % 4) return fail(LSK_EINVAL, "r must be a multiple of 4");
+  if (n < 1 || p->d < 1) return fail(LSK_EINVAL, "n and d must be >= 1");
+  if (s_degree < 0 || s_degree > 2) return fail(LSK_EINVAL, "s must be 0, 1 or 2");
+  if (!(kappa > 0.0)) return fail(LSK_EINVAL, "kappa must be > 0");
+  if (!(p->sigma > 1.0)) return fail(LSK_EDOMAIN, "the arc-cosine map needs sigma > 1");
+  if (!aligned16(Xi)) return fail(LSK_EINVAL, "Xi must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool tensor = p->d > 16;
+  char* ws;
+  Carve cv;
+  const size_t oC = cv.take(sizeof(float) * p->r);
+  const size_t oI = tensor ? cv.take(feature_map_tc_image_bytes(p->r, p->d)) : 0;
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  float* coef = reinterpret_cast<float*>(ws + oC);
+  LSK_CU(launch_arccos_coef(U, p->r, p->d, p->sigma, coef, s));
+  if (tensor) {
+    LSK_CU(launch_feature_map_tc(X, n, p->d, U, coef, p->r, 1.0, reinterpret_cast<float*>(ws + oI),
+                                 Xi, s, 1, s_degree, p->r + 4));
+    LSK_CU(launch_const_cols(Xi, n, p->r + 4, p->r, (float)std::sqrt(kappa), s));
+  } else {
+    LSK_CU(launch_feature_map_arccos(X, n, p->d, U, coef, p->r, s_degree, kappa, Xi, s));
+  }
+  return LSK_OK;
+}
+
 lsk_status lsk_feature_map_batched(const lsk_feature_params* p, const float* U, const float* X,
                                    int64_t n, int32_t batch, float* Xi, void* stream) {
   if (batch < 1) return fail(LSK_EINVAL, "batch must be >= 1");

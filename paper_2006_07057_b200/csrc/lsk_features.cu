@@ -243,6 +243,102 @@ cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- NEXT f3: arc-cosine ---
+// Xi[i][k] = coef_k relu(u_k . x_i)^s (k < r), Xi[i][r] = sqrt(kappa), Xi[i][r+1..r+3] = 0,
+// coef_k = sigma^{d/2} sqrt(2) exp(-|u_k|^2/4 (1 - 1/sigma^2)) / sqrt(r).
+__global__ void arccos_coef_kernel(const float* __restrict__ U, int r, int d, double sigma,
+                                   float* coef) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= r) return;
+  double uu = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double v = (double)U[(int64_t)k * d + c];
+    uu += v * v;
+  }
+  coef[k] = (float)(pow(sigma, 0.5 * d) * sqrt(2.0) * exp(-uu / 4.0 * (1.0 - 1.0 / (sigma * sigma))) /
+                    sqrt((double)r));
+}
+
+__device__ __forceinline__ float relu_pow(float t, int sdeg) {
+  if (sdeg == 0) return t > 0.f ? 1.f : 0.f;
+  const float rl = fmaxf(t, 0.f);
+  return sdeg == 1 ? rl : rl * rl;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) arccos_direct_kernel(
+    const float* __restrict__ X, int64_t n, const float* __restrict__ U,
+    const float* __restrict__ coef, int r, int sdeg, float sqrt_kappa, float* __restrict__ Xi) {
+  constexpr int RB = 32;
+  __shared__ float xs[RB][D];
+  const int64_t row0 = (int64_t)blockIdx.x * RB;
+  const int rows = (int)min((int64_t)RB, n - row0);
+  for (int i = threadIdx.x; i < rows * D; i += blockDim.x) xs[i / D][i % D] = X[row0 * D + i];
+  __syncthreads();
+  const int ld = r + 4, R4 = r >> 2;
+  for (int g = threadIdx.x; g <= R4; g += blockDim.x) {
+    if (g == R4) {   // the collapsed kappa slot + zero padding
+      for (int i = 0; i < rows; ++i)
+        st_global_cs(reinterpret_cast<float4*>(Xi + (row0 + i) * ld) + g, make_float4(sqrt_kappa, 0.f, 0.f, 0.f));
+      continue;
+    }
+    float u[4][D];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[q][c] = U[(int64_t)(4 * g + q) * D + c];
+    const float4 cf = *reinterpret_cast<const float4*>(coef + 4 * g);
+    const float cq[4] = {cf.x, cf.y, cf.z, cf.w};
+    for (int i = 0; i < rows; ++i) {
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float t = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) t = fmaf(u[q][c], xs[i][c], t);
+        o[q] = cq[q] * relu_pow(t, sdeg);
+      }
+      st_global_cs(reinterpret_cast<float4*>(Xi + (row0 + i) * ld) + g, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+__global__ void const_cols_kernel(float* Xi, int64_t n, int ld, int col, float val) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n)
+    *reinterpret_cast<float4*>(Xi + i * ld + col) = make_float4(val, 0.f, 0.f, 0.f);
+}
+
+cudaError_t launch_arccos_coef(const float* U, int r, int d, double sigma, float* coef,
+                               cudaStream_t s) {
+  arccos_coef_kernel<<<(r + 127) / 128, 128, 0, s>>>(U, r, d, sigma, coef);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_feature_map_arccos(const float* X, int64_t n, int d, const float* U,
+                                      const float* coef, int r, int sdeg, double kappa,
+                                      float* Xi, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)((n + 31) / 32);
+  const float sk = (float)sqrt(kappa);
+  switch (d) {
+#define CASE(DD) case DD: arccos_direct_kernel<DD><<<blocks, 256, 0, s>>>(X, n, U, coef, r, sdeg, sk, Xi); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_const_cols(float* Xi, int64_t n, int ld, int col, float val, cudaStream_t s) {
+  const_cols_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(Xi, n, ld, col, val);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- a9: read-out -----------
 // partials[(prob * 2 + side) * B + blk] = sum over the block's fixed range of c ln w
 constexpr int kRotBlocks = 64;

@@ -75,12 +75,11 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 
 // W hi/lo images: [ntile][kchunk][2][BN rows x 128 B swizzled]; rows >= r and k >= d are 0.
-__global__ void w_images_kernel(const float* __restrict__ U, int r, int d, double eps,
+__global__ void w_images_kernel(const float* __restrict__ U, int r, int d, double sc,
                                 float* __restrict__ img) {
   const int nt = blockIdx.x, kc = blockIdx.y;
   const int nkc = gridDim.y;
   char* base = reinterpret_cast<char*>(img) + ((size_t)nt * nkc + kc) * 2 * kWBytes;
-  const double sc = 4.0 * kLog2e / eps;
   for (int i = threadIdx.x; i < BN * BK; i += blockDim.x) {
     const int row = i / BK, k = i % BK;
     const int n = nt * BN + row, c = kc * BK + k;
@@ -92,9 +91,12 @@ __global__ void w_images_kernel(const float* __restrict__ U, int r, int d, doubl
   }
 }
 
+// mode 0 (Gaussian): out = 2^(alpha2 + beta2_k + acc); mode 1 (arc-cosine): out =
+// beta2_k relu(acc)^sdeg with beta2 = the per-anchor coefficient.  Output row stride ld.
 __global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
     const float* __restrict__ X, int64_t M, int d, const float* __restrict__ wimg,
-    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi) {
+    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int mode,
+    int sdeg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -225,16 +227,22 @@ __global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (orow < M) {
-      float* dst = Xi + orow * r + n0 + col;
+      float* dst = Xi + orow * ld + n0 + col;
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
         if (n0 + col + j < r) {
-          float4 o;
-          o.x = ex2(al + beta_s[col + j + 0] + __uint_as_float(a[j + 0]));
-          o.y = ex2(al + beta_s[col + j + 1] + __uint_as_float(a[j + 1]));
-          o.z = ex2(al + beta_s[col + j + 2] + __uint_as_float(a[j + 2]));
-          o.w = ex2(al + beta_s[col + j + 3] + __uint_as_float(a[j + 3]));
-          st_global_cs(reinterpret_cast<float4*>(dst + j), o);
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float acc = __uint_as_float(a[j + e]);
+            if (mode == 0) {
+              o[e] = ex2(al + beta_s[col + j + e] + acc);
+            } else {
+              const float rl = fmaxf(acc, 0.f);
+              o[e] = beta_s[col + j + e] * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
+            }
+          }
+          st_global_cs(reinterpret_cast<float4*>(dst + j), make_float4(o[0], o[1], o[2], o[3]));
         }
       }
     }
@@ -257,17 +265,20 @@ size_t feature_map_tc_image_bytes(int r, int d) {
 
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
                                   const float* beta2, int r, double eps, float* wimg, float* Xi,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, int mode, int sdeg, int ld) {
   if (n <= 0) return cudaSuccess;
+  if (ld <= 0) ld = r;
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
-  tc::w_images_kernel<<<dim3(nt, nkc), 256, 0, s>>>(U, r, d, eps, wimg);
+  const double wscale = mode == 0 ? 4.0 * tc::kLog2e / eps : 1.0;
+  tc::w_images_kernel<<<dim3(nt, nkc), 256, 0, s>>>(U, r, d, wscale, wimg);
   count_launch();
   cudaError_t e = cudaFuncSetAttribute(tc::feature_map_tc_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
   if (e != cudaSuccess) return e;
   const float c2 = (float)(-2.0 * tc::kLog2e / eps);
   dim3 grid((unsigned)((n + tc::BM - 1) / tc::BM), (unsigned)nt);
-  tc::feature_map_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi);
+  tc::feature_map_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi,
+                                                                        ld, mode, sdeg);
   count_launch();
   return cudaGetLastError();
 }

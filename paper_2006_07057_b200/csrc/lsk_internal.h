@@ -95,7 +95,14 @@ cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
 size_t feature_map_tc_image_bytes(int r, int d);
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
                                   const float* beta2, int r, double eps, float* wimg, float* Xi,
-                                  cudaStream_t s);
+                                  cudaStream_t s, int mode = 0, int sdeg = 0, int ld = 0);
+// arc-cosine features (NEXT f3)
+cudaError_t launch_arccos_coef(const float* U, int r, int d, double sigma, float* coef,
+                               cudaStream_t s);
+cudaError_t launch_feature_map_arccos(const float* X, int64_t n, int d, const float* U,
+                                      const float* coef, int r, int sdeg, double kappa,
+                                      float* Xi, cudaStream_t s);
+cudaError_t launch_const_cols(float* Xi, int64_t n, int ld, int col, float val, cudaStream_t s);
 // envelope gradients (lsk_grad.cu)
 size_t grad_workspace_bytes(int r, int d);
 cudaError_t launch_gradients(const float* X, int64_t n, const float* Y, int64_t m, int d,

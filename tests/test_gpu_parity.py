@@ -378,3 +378,40 @@ def test_envelope_gradients(L, cfg_key, n, m):
         want = gref[key]
         err = np.abs(got - want).max() / np.abs(want).max()
         assert err <= 2e-4, (k, err)
+
+
+# ------------------------------------------------------------------ NEXT f3: arc-cosine ----
+@pytest.mark.parametrize("d,s_deg,n", [(3, 1, 1031), (2, 0, 777), (16, 2, 513), (128, 1, 700)])
+def test_arccos_features_and_solve(L, d, s_deg, n):
+    """Arc-cosine features (Lemma decomp-arccos) vs the oracle entry by entry,
+    then Alg. 1 on those factors (rank r + 1, padded to r + 4) vs the oracle's Sinkhorn."""
+    import torch
+    r, sigma, kappa, eps, T = 256, 1.5, 0.1, 0.5, 150
+    rng = np.random.default_rng(100 + d)
+    X = (rng.normal(size=(n, d)) / math.sqrt(d)).astype(np.float32)
+    Y = (rng.normal(0.2, 1.0, size=(n + 7, d)) / math.sqrt(d)).astype(np.float32)
+    a = np.full(n, 1.0 / n, np.float32)
+    b = np.full(n + 7, 1.0 / (n + 7), np.float32)
+    p = L.arccos_params(d, r, sigma, 77, eps)
+    U = torch.empty((r, d), device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((n, r + 4), device="cuda")
+    Ze = torch.empty((n + 7, r + 4), device="cuda")
+    L.lsk_feature_map_arccos(p, s_deg, kappa, U, _dev(X), Xi)
+    L.lsk_feature_map_arccos(p, s_deg, kappa, U, _dev(Y), Ze)
+    Uo = O.draw_anchors(r, d, sigma, 77)
+    fx = O.feature_matrix_arccos(X, Uo, sigma, s_deg, kappa)       # (r+1) x n, paper layout
+    fy = O.feature_matrix_arccos(Y, Uo, sigma, s_deg, kappa)
+    got = Xi.cpu().double().numpy()
+    assert np.all(got[:, r + 1:] == 0)
+    ref = fx.T
+    tol = 1e-5 if d <= 16 else 2e-4
+    err = np.abs(got[:, :r + 1] - ref) / (np.abs(ref) + 1e-3 * ref.max())
+    assert err.max() <= tol, err.max()
+    u = torch.empty(n, device="cuda")
+    v = torch.empty(n + 7, device="cuda")
+    rep = L.lsk_factored_sinkhorn(Xi, Ze, _dev(a), _dev(b), eps, L.make_opts(T), u, v)
+    sol = O.sinkhorn_factored(fx, fy, a, b, T=T)
+    rot_ref = O.dual_estimate(sol["u"], sol["v"], a, b, eps)
+    assert abs(rep.rot - rot_ref) <= ROT_TOL * abs(rot_ref)
+    assert _maxrel(u, sol["u"]) <= UV_TOL and _maxrel(v, sol["v"]) <= UV_TOL

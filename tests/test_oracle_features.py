@@ -204,3 +204,56 @@ def test_anchor_moments_and_prefix():
     assert np.array_equal(U1, U2[:100])          # prefix property
     assert not np.array_equal(U1, O.draw_anchors(100, 3, 0.4, 78))
     assert abs(U2.std() / 0.4 - 1) < 0.05
+
+
+# ---------------- NEXT f3: arc-cosine perturbed features (reading C21) ---------
+@pytest.mark.parametrize("s", [0, 1, 2])
+def test_arccos_kernel_identity_quadrature(s):
+    """int phi(x,u)^T phi(y,u) d rho(u) = k_s(x,y) + kappa with rho = N(0, sigma^2 I), sigma > 1
+    (Lemma decomp-arccos), k_s the closed-form arc-cosine kernel (Cho & Saul).  The map is
+    integrated as written (arccos_phi) in polar coordinates, d = 2: Gauss-Legendre over the
+    exact arc where both u^T x > 0 and u^T y > 0 (elsewhere the first slot is 0 and only the
+    kappa slot contributes kappa * rho-mass), Gauss-Legendre over the radius in [0, 12 sigma]."""
+    sigma, kappa = 1.5, 0.1
+    x, y = np.array([0.8, 0.3]), np.array([-0.2, 0.9])
+    ax, ay = math.atan2(x[1], x[0]), math.atan2(y[1], y[0])
+    # u^T x > 0  <=>  angle in (ax - pi/2, ax + pi/2); intersect with the arc for y
+    lo, hi = max(ax, ay) - math.pi / 2, min(ax, ay) + math.pi / 2
+    tn, tw = np.polynomial.legendre.leggauss(200)
+    t = 0.5 * (hi - lo) * tn + 0.5 * (hi + lo)
+    tw = 0.5 * (hi - lo) * tw
+    rn, rw = np.polynomial.legendre.leggauss(400)
+    L = 12 * sigma
+    rho = 0.5 * L * (rn + 1)
+    rw = 0.5 * L * rw
+    T, Rr = np.meshgrid(t, rho, indexing="ij")
+    W = np.outer(tw, rw) * Rr * np.exp(-Rr ** 2 / (2 * sigma ** 2)) / (2 * math.pi * sigma ** 2)
+    U = np.stack([Rr * np.cos(T), Rr * np.sin(T)], axis=-1)
+    first = O.arccos_phi(x, U, sigma, s, kappa)[..., 0] * O.arccos_phi(y, U, sigma, s, kappa)[..., 0]
+    integral = float((first * W).sum()) + kappa
+    exact = O.arccos_kernel(x, y, s) + kappa
+    assert abs(integral / exact - 1) < 1e-10, (integral, exact)
+
+
+def test_arccos_kernel_closed_form_special_cases():
+    """k_0(x,x) = 1, k_1(x,x) = |x|^2, k_1(x,-x) = 0, orthogonal k_1 = |x||y|/pi."""
+    x = np.array([0.6, 0.8])
+    assert abs(O.arccos_kernel(x, x, 0) - 1.0) < 1e-15
+    assert abs(O.arccos_kernel(x, x, 1) - 1.0) < 1e-15
+    assert abs(O.arccos_kernel(x, -x, 1)) < 1e-7
+    assert abs(O.arccos_kernel(np.array([2.0, 0.0]), np.array([0.0, 3.0]), 1) - 6 / math.pi) < 1e-14
+
+
+def test_arccos_feature_matrix_and_mc():
+    sigma, kappa, s, r = 1.5, 0.1, 1, 20000
+    U = O.draw_anchors(r, 3, sigma, 5)
+    rng = np.random.default_rng(2)
+    X = rng.normal(size=(4, 3)) * 0.5
+    F = O.feature_matrix_arccos(X, U, sigma, s, kappa)
+    assert F.shape == (r + 1, 4) and np.all(F >= 0)
+    Kt = F.T @ F
+    for i in range(4):
+        for j in range(4):
+            exact = O.arccos_kernel(X[i], X[j], s) + kappa
+            assert abs(Kt[i, j] / exact - 1) < 0.05
+            assert Kt[i, j] >= kappa
