@@ -276,6 +276,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   }
   A.gpp = c.gpp;
   A.dbg = getenv("LSK_DEBUG") ? atoi(getenv("LSK_DEBUG")) : 0;
+  A.l2_resident = getenv("LSK_L2RES") ? (float)atof(getenv("LSK_L2RES")) : 0.f;   // tuning knob
   A.nprob = batch;
   A.nstage = c.nstage;
   A.stage_floats = c.stage_floats;

@@ -43,15 +43,18 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   constexpr int NWT = TS / 32;         // warps per team
   constexpr int NW = NT / 32;
   constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;
-  static_assert(TEAMS == 1 || TEAMS == 2, "1 or 2 teams");
+  static_assert(TEAMS == 1 || TEAMS == 2 || TEAMS == 4, "1, 2 or 4 teams");
   __shared__ __align__(16) Smem<TS, TEAMS> S;
-  __shared__ double comb[TEAMS > 1 ? TS : 1][TEAMS > 1 ? NV * 4 : 1];
+  // fp64 accumulators of every thread in shared memory (touched once per kFlushTiles tiles):
+  // element-major so consecutive threads hit consecutive words
+  extern __shared__ double acc_dyn[];   // dynamic: [NV * 4][NT]
+  double (*acc_s)[NT] = reinterpret_cast<double (*)[NT]>(acc_dyn);
 
   const int tid = threadIdx.x;
   const int team = tid / TS, ttid = tid - team * TS;
   const int warp = tid >> 5, lane = tid & 31;
   const int twarp = ttid >> 5;          // warp index within the team
-  const uint32_t team_bar = 2u + (uint32_t)team;
+  const uint32_t team_bar = 2u + (uint32_t)team;   // ids 2..5 (1 = whole CTA)
   const int prob = blockIdx.x / A.gpp;
   const int cta = blockIdx.x - prob * A.gpp;
   const int r = A.r;
@@ -82,12 +85,11 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   __syncthreads();
 
   float4 s[NV];
-  double acc64[NV][4];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+    for (int q = 0; q < 4; ++q) acc_s[j * 4 + q][tid] = 0.0;
   }
 
   double stErr = __ldcg(stg_state + ST_ERR);
@@ -150,24 +152,17 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j]));
           const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j] + 2));
           s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
-        } else {   // gpp == 1: the combined accumulator is in team 0 (and in comb for team 1)
-          if constexpr (TEAMS > 1) {
-            if (team == 1)
-              s[j] = make_float4((float)comb[ttid][j * 4], (float)comb[ttid][j * 4 + 1],
-                                 (float)comb[ttid][j * 4 + 2], (float)comb[ttid][j * 4 + 3]);
-            else
-              s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
-          } else {
-            s[j] = make_float4((float)acc64[j][0], (float)acc64[j][1], (float)acc64[j][2], (float)acc64[j][3]);
-          }
+        } else {   // gpp == 1: the combined accumulator sits in team 0's slots
+          s[j] = make_float4((float)acc_s[j * 4][ttid], (float)acc_s[j * 4 + 1][ttid],
+                             (float)acc_s[j * 4 + 2][ttid], (float)acc_s[j * 4 + 3][ttid]);
         }
       }
-      if constexpr (TEAMS > 1) named_bar(1, NT);   // comb reads done before it is rewritten
+      named_bar(1, NT);   // every team has read team 0's slots before they are cleared
     }
 #pragma unroll
     for (int j = 0; j < NV; ++j)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
+      for (int q = 0; q < 4; ++q) acc_s[j * 4 + q][tid] = 0.0;
 
     int64_t r0, r1;
     cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
@@ -272,7 +267,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
         for (int w = 0; w < NWT; ++w) tt += S.red[team][rb][w][lane];   // fixed order
         const float c = sl[lane];
         if (kind != PK_ERR) vr_l = __fdiv_rn(c, tt);
-        if (twarp == 0) {
+        if (twarp == NWT - 1) {   // the loader is warp 0: outputs go to the last warp
           if (kind == PK_ERR || (kind == PK_V && p >= 3))
             errsum += fabs((double)sl[32 + lane] * (double)tt - (double)c);
           if (kind != PK_ERR) {
@@ -297,10 +292,10 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           tiles_since_flush = 0;
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            acc64[j][0] += (double)acc32[j].x;
-            acc64[j][1] += (double)acc32[j].y;
-            acc64[j][2] += (double)acc32[j].z;
-            acc64[j][3] += (double)acc32[j].w;
+            acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
+            acc_s[j * 4 + 1][tid] += (double)acc32[j].y;
+            acc_s[j * 4 + 2][tid] += (double)acc32[j].z;
+            acc_s[j * 4 + 3][tid] += (double)acc32[j].w;
             acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
@@ -309,38 +304,43 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     if (twarp == 0) cp_async_wait<0>();
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      acc64[j][0] += (double)acc32[j].x;
-      acc64[j][1] += (double)acc32[j].y;
-      acc64[j][2] += (double)acc32[j].z;
-      acc64[j][3] += (double)acc32[j].w;
+      acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
+      acc_s[j * 4 + 1][tid] += (double)acc32[j].y;
+      acc_s[j * 4 + 2][tid] += (double)acc32[j].z;
+      acc_s[j * 4 + 3][tid] += (double)acc32[j].w;
     }
 
     // ---------------- end of pass: teams combined (fixed order), cross-CTA fp64 reduction ---
     double e0 = 0.0, e1 = 0.0;
-    if (twarp == 0) {
+    if (twarp == NWT - 1) {
       e0 = warp_sum_f64(errsum);
       e1 = warp_sum_f64(brksum);
     }
+    if (twarp == NWT - 1 && lane == 0) {   // hand the team's extras to its thread 0
+      S.xs[0][NW - 1 - team] = e0;
+      S.xs[1][NW - 1 - team] = e1;
+    }
+    named_bar(1, NT);
+    if (ttid == 0) {
+      e0 = S.xs[0][NW - 1 - team];
+      e1 = S.xs[1][NW - 1 - team];
+    }
+    named_bar(1, NT);
     if constexpr (TEAMS > 1) {
-      if (team == 1) {
-#pragma unroll
-        for (int j = 0; j < NV; ++j)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) comb[ttid][j * 4 + q] = acc64[j][q];
-        if (ttid == 0) {
-          S.xs[0][0] = e0;
-          S.xs[1][0] = e1;
-        }
+      if (team > 0 && ttid == 0) {
+        S.xs[0][team] = e0;
+        S.xs[1][team] = e1;
       }
       named_bar(1, NT);
-      if (team == 0) {
+      if (team == 0) {   // fixed order: team 0 + team 1 + ... (deterministic)
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
+        for (int tm = 1; tm < TEAMS; ++tm) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc64[j][q] += comb[ttid][j * 4 + q];
-        if (ttid == 0) {
-          e0 += S.xs[0][0];
-          e1 += S.xs[1][0];
+          for (int e = 0; e < NV * 4; ++e) acc_s[e][ttid] += acc_s[e][ttid + tm * TS];
+          if (ttid == 0) {
+            e0 += S.xs[0][tm];
+            e1 += S.xs[1][tm];
+          }
         }
       }
       named_bar(1, NT);
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[(int64_t)(4 * g[j] + q) * A.gpp + cta] = acc64[j][q];
+            for (int q = 0; q < 4; ++q) part[(int64_t)(4 * g[j] + q) * A.gpp + cta] = acc_s[j * 4 + q][ttid];
           }
         }
       }
@@ -377,14 +377,6 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       if (!multi) group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[3] = globaltimer();
     } else {
-      if constexpr (TEAMS > 1) {
-        if (team == 0) {
-#pragma unroll
-          for (int j = 0; j < NV; ++j)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) comb[ttid][j * 4 + q] = acc64[j][q];
-        }
-      }
       if (tid == 0) {
         S.ext[0] = e0;
         S.ext[1] = e1;
@@ -464,8 +456,11 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 void implicit_config(int r, int* nt, int* nv, int* tr) {
   const int r4 = (r + 3) / 4;
   if (r4 <= 256) {
-    *nt = 256; *nv = 1; *tr = 8;
-    if (const char* e = getenv("LSK_ITR")) *tr = atoi(e) == 16 ? 16 : 8;   // tuning knob
+    // four 128-thread teams, 8 columns per thread (halves the per-entry exchange overhead)
+    *nt = 128; *nv = 2; *tr = 4;
+    if (const char* e = getenv("LSK_ITEAM")) {   // tuning knob: 2 = two 256-thread teams
+      if (atoi(e) == 2) { *nt = 256; *nv = 1; *tr = 8; }
+    }
   }
   else if (r4 <= 512) { *nt = 512; *nv = 1; *tr = 8; }
   else { *nt = 512; *nv = 2; *tr = 2; }
@@ -474,7 +469,7 @@ void implicit_config(int r, int* nt, int* nv, int* tr) {
 #define LSK_IMPL2(X, TS, TM, NV, TR) X(TS, TM, NV, TR, 1) X(TS, TM, NV, TR, 2) \
   X(TS, TM, NV, TR, 3) X(TS, TM, NV, TR, 4) X(TS, TM, NV, TR, 5) X(TS, TM, NV, TR, 6)     \
   X(TS, TM, NV, TR, 7) X(TS, TM, NV, TR, 8)
-#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 256, 2, 1, 16) LSK_IMPL2(X, 512, 1, 1, 8) \
+#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 128, 4, 2, 4) LSK_IMPL2(X, 512, 1, 1, 8) \
   LSK_IMPL2(X, 512, 1, 2, 2)
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
@@ -483,12 +478,14 @@ cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t
 #define X(TS_, TM_, NV_, TR_, D_)                                                              \
   if (ts == TS_ && nv == NV_ && tr == TR_ && a.d == D_) {                                      \
     auto kern = impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>;                                 \
-    cudaError_t e;                                                                             \
+    const size_t dyn = sizeof(double) * NV_ * 4 * TS_ * TM_;                                   \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn); \
+    if (e != cudaSuccess) return e;                                                            \
     if (coop) {                                                                                \
       void* args[] = {(void*)&a};                                                              \
-      e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS_ * TM_), args, 0, s); \
+      e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS_ * TM_), args, dyn, s); \
     } else {                                                                                   \
-      kern<<<grid, TS_ * TM_, 0, s>>>(a);                                                      \
+      kern<<<grid, TS_ * TM_, dyn, s>>>(a);                                                    \
       e = cudaGetLastError();                                                                  \
     }                                                                                          \
     count_launch();                                                                            \
@@ -505,7 +502,10 @@ int implicit_max_ctas_per_sm(int r, int d) {
 #define X(TS_, TM_, NV_, TR_, D_)                                                              \
   if (ts == TS_ && nv == NV_ && tr == TR_ && d == D_) {                                        \
     int nb = 0;                                                                                \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>, TS_ * TM_, 0); \
+    const size_t dyn = sizeof(double) * NV_ * 4 * TS_ * TM_;                                   \
+    cudaFuncSetAttribute(impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>,                        \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);               \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>, TS_ * TM_, dyn); \
     return nb;                                                                                 \
   }
   LSK_IMPL2_ALL(X)

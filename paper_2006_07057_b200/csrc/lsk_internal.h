@@ -63,6 +63,7 @@ struct SinkArgs {
   float c2;                // -2 log2e / eps
   int dbg;                 // tuning only: 1 = consumers release stages without computing
   unsigned long long* trace;   // tuning only: [pass][cta][4] globaltimer stamps, or NULL
+  float l2_resident;       // fraction of each CTA's rows per factor kept L2-resident (evict_last)
   int tr;                  // rows per tile (template dispatch)
   int nv;                  // float4 column groups per consumer thread (template dispatch)
 };

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   if (warp == NW) {
     uint32_t stage = 0, phase = 0;
     const uint64_t pol = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
     for (int p = A.pass_begin; p < A.pass_end; ++p) {
       const int kind = pass_kind(p, A);
       if (kind == PK_NONE) continue;
@@ -107,6 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (need_vold) vold = vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1);
       const float* Fp = IMPL ? nullptr : A.F[f] + (int64_t)prob * A.fstride[f];
       const float* Xp = IMPL ? A.X[f] + (int64_t)prob * A.fstride[f] : nullptr;
+      // the first l2_resident of this CTA's rows stay in L2 across iterations (evict_last)
+      const int64_t keep_end = r0 + (int64_t)((double)(r1 - r0) * (double)A.l2_resident);
       for (int64_t row0 = r0; row0 < r1; row0 += TR) {
         const int rows = (int)min((int64_t)TR, r1 - row0);
         mbar_wait(&S.empty[stage], phase ^ 1u);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
           if constexpr (!IMPL) {
             const uint32_t bytes = (uint32_t)rows * (uint32_t)r * 4u;
             mbar_arrive_expect_tx(&S.full[stage], bytes);
-            bulk_g2s(st + kHdr, Fp + row0 * r, bytes, &S.full[stage], pol);
+            bulk_g2s(st + kHdr, Fp + row0 * r, bytes, &S.full[stage], row0 < keep_end ? pol_keep : pol);
           } else {
             mbar_arrive(&S.full[stage]);
           }
