@@ -137,7 +137,7 @@ def run_reference(args):
         t_feat_all.append(t_feat)
         t_iter_all.append(t_it)
         step_vals.append(cfg.T / (t_feat + cfg.T * t_it))
-    cores = sum(int(i.get("num_threads", 0)) for i in threadpool_info()) or os.cpu_count()
+    cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] or [os.cpu_count()])
     value = float(np.median(step_vals))
     sample = ("config %d full size (n=m=%d, r=%d): fp64 features + %d of T=%d iterations per "
               "step, extrapolated to T" % (cfg.key, cfg.n, cfg.r, k_iter, cfg.T))
@@ -175,7 +175,7 @@ def cpu_baseline(cfg, iters=3):
     t2 = time.perf_counter()
     t_it = (t2 - t1) / iters
     value = cfg.T / ((t1 - t0) + cfg.T * t_it)
-    cores = sum(int(i.get("num_threads", 0)) for i in threadpool_info()) or os.cpu_count()
+    cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] or [os.cpu_count()])
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": "config %d full size: fp64 features + %d of T=%d iterations, extrapolated "
                       "to T (features %.2f s, %.3f s/iteration)" % (cfg.key, iters, cfg.T,
@@ -295,10 +295,10 @@ def run_lsk(args):
     else:
         ex2 = float(r) * (n_loc + T * (n_loc + m_loc))
         achieved = ex2 / (kmean / 1e3) / 1e9
-        peak = 16.0 * 148 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        peak = 4626.0   # measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gex2/s",
                 "frac": achieved / peak, "traffic": None,
-                "peak_source": "MUFU ex2: 16/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md)",
+                "peak_source": "MUFU ex2 measured on B200 (profiles/r01_mufu_microbench.txt)",
                 "algorithmic_ex2_per_launch": ex2}
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):

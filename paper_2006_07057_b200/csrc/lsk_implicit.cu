@@ -463,14 +463,17 @@ void implicit_config(int r, int* nt, int* nv, int* tr) {
     }
   }
   else if (r4 <= 512) { *nt = 512; *nv = 1; *tr = 8; }
-  else { *nt = 512; *nv = 2; *tr = 2; }
+  else {
+    *nt = 512; *nv = 2; *tr = 4;
+    if (const char* e = getenv("LSK_ITR")) *tr = atoi(e) == 2 ? 2 : 4;   // tuning knob
+  }
 }
 
 #define LSK_IMPL2(X, TS, TM, NV, TR) X(TS, TM, NV, TR, 1) X(TS, TM, NV, TR, 2) \
   X(TS, TM, NV, TR, 3) X(TS, TM, NV, TR, 4) X(TS, TM, NV, TR, 5) X(TS, TM, NV, TR, 6)     \
   X(TS, TM, NV, TR, 7) X(TS, TM, NV, TR, 8)
 #define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 128, 4, 2, 4) LSK_IMPL2(X, 512, 1, 1, 8) \
-  LSK_IMPL2(X, 512, 1, 2, 2)
+  LSK_IMPL2(X, 512, 1, 2, 2) LSK_IMPL2(X, 512, 1, 2, 4)
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
   int ts, nv, tr;
