@@ -210,8 +210,9 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       const float* sl = S.slot[team][t % kRing];
       if (twarp == 0) issue(t + 2);   // slot (t+2)%4 was last read in tile t-2 (< previous barrier)
 
-      // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero data)
-      float fr[TR][NV][4];
+      // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero data);
+      // packed fp32x2 arithmetic (FFMA2/FADD2): two columns per instruction
+      float2 fr[TR][NV][2];
 #pragma unroll
       for (int i = 0; i < TR; ++i) {
         float x[D];
@@ -221,20 +222,19 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 #pragma unroll
         for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
         al *= A.c2;
+        const float2 al2 = make_float2(al, al);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          float e0 = al + b2[j].x, e1 = al + b2[j].y, e2 = al + b2[j].z, e3 = al + b2[j].w;
+          float2 e01 = add2(al2, make_float2(b2[j].x, b2[j].y));
+          float2 e23 = add2(al2, make_float2(b2[j].z, b2[j].w));
 #pragma unroll
           for (int c = 0; c < D; ++c) {
-            e0 = fmaf(Wr[j][c].x, x[c], e0);
-            e1 = fmaf(Wr[j][c].y, x[c], e1);
-            e2 = fmaf(Wr[j][c].z, x[c], e2);
-            e3 = fmaf(Wr[j][c].w, x[c], e3);
+            const float2 xc = make_float2(x[c], x[c]);
+            e01 = fma2(make_float2(Wr[j][c].x, Wr[j][c].y), xc, e01);
+            e23 = fma2(make_float2(Wr[j][c].z, Wr[j][c].w), xc, e23);
           }
-          fr[i][j][0] = ex2(e0);
-          fr[i][j][1] = ex2(e1);
-          fr[i][j][2] = ex2(e2);
-          fr[i][j][3] = ex2(e3);
+          fr[i][j][0] = make_float2(ex2(e01.x), ex2(e01.y));
+          fr[i][j][1] = make_float2(ex2(e23.x), ex2(e23.y));
         }
       }
       const int rb = t & 1;
@@ -242,14 +242,13 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
         float pr[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
-          pr[i] = 0.f;
+          float2 pp = make_float2(0.f, 0.f);
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            pr[i] = fmaf(fr[i][j][0], s[j].x, pr[i]);
-            pr[i] = fmaf(fr[i][j][1], s[j].y, pr[i]);
-            pr[i] = fmaf(fr[i][j][2], s[j].z, pr[i]);
-            pr[i] = fmaf(fr[i][j][3], s[j].w, pr[i]);
+            pp = fma2(fr[i][j][0], make_float2(s[j].x, s[j].y), pp);
+            pp = fma2(fr[i][j][1], make_float2(s[j].z, s[j].w), pp);
           }
+          pr[i] = pp.x + pp.y;
         }
         const float tot = warp_transpose_reduce<TR>(pr, lane);
         constexpr int kLanesPerRow = 32 / TR;
@@ -280,12 +279,12 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
           const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+          const float2 v2 = make_float2(vi, vi);
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
-            acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
-            acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
-            acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
+            const float2 lo = fma2(fr[i][j][0], v2, make_float2(acc32[j].x, acc32[j].y));
+            const float2 hi = fma2(fr[i][j][1], v2, make_float2(acc32[j].z, acc32[j].w));
+            acc32[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
           }
         }
         if (++tiles_since_flush == kFlushTiles) {

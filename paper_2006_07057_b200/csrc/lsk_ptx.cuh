@@ -113,6 +113,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// ---- packed fp32x2 (Blackwell FFMA2 / FADD2: two fp32 lanes per instruction, same rate) --
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) {
+  return *reinterpret_cast<unsigned long long*>(&v);
+}
+__device__ __forceinline__ float2 bits_f2(unsigned long long b) {
+  return *reinterpret_cast<float2*>(&b);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+
 // ---- MUFU ex2 (2^x, flush-to-zero; rel. err ~2^-22) --------------------------------------
 __device__ __forceinline__ float ex2(float x) {
   float y;
