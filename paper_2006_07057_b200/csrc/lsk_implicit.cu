@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "lsk_internal.h"
 #include "lsk_ptx.cuh"
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
     const float* Xp = A.X[f] + (int64_t)prob * A.fstride[f];
     const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
+    const bool err_here = need_vold;
     const float* vold = need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) : nullptr;
     float* outp = nullptr;
     if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
@@ -179,126 +181,144 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     float4 acc32[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int tiles_since_flush = 0;
 
-    // warp 0 stages tile t (point rows + c_j + v_old_j) into slot t % kRing.  v_old_j was
-    // written by this same lane two passes earlier (same tiling), so no extra ordering.
-    auto issue = [&](int t) {
-      if (t < ntiles) {
-        const int64_t row0 = r0 + (int64_t)(team + t * TEAMS) * TR;
-        const int rows = (int)min((int64_t)TR, r1 - row0);
-        float* sl = S.slot[team][t % kRing];
-        if (lane < rows) {
-          cp_async4(sl + lane, wp + row0 + lane);
-          if (need_vold) cp_async4(sl + 32 + lane, vold + row0 + lane);
+    // The tile loop is instantiated per pass kind (compile-time KIND: no per-tile kind
+    // branches) with 32-bit row offsets relative to this CTA's first row.
+    const int nrows = (int)(r1 - r0);
+    const float* wp0 = wp + r0;
+    const float* vold0 = need_vold ? vold + r0 : nullptr;
+    const float* Xp0 = Xp + r0 * D;
+    float* outp0 = outp ? outp + r0 : nullptr;
+
+    auto run_tiles = [&](auto kind_tag) {
+      constexpr int KIND = decltype(kind_tag)::value;
+      constexpr bool kDot = KIND != PK_INIT;
+      constexpr bool kAcc = KIND != PK_ERR;
+      constexpr bool kOut = KIND == PK_U || KIND == PK_V;
+      // warp 0 stages tile t (point rows + c_j + v_old_j) into slot t % kRing.  v_old_j was
+      // written by this same lane two passes earlier (same tiling), so no extra ordering.
+      auto issue = [&](int t) {
+        if (t < ntiles) {
+          const int lr = (team + t * TEAMS) * TR;
+          float* sl = S.slot[team][t & (kRing - 1)];
+          if (lane < nrows - lr && lane < TR) {
+            cp_async4(sl + lane, wp0 + lr + lane);
+            if (need_vold) cp_async4(sl + 32 + lane, vold0 + lr + lane);
 #pragma unroll
-          for (int c = 0; c < D; ++c) cp_async4(sl + 64 + lane * 8 + c, Xp + (row0 + lane) * D + c);
+            for (int c = 0; c < D; ++c) cp_async4(sl + 64 + lane * 8 + c, Xp0 + (lr + lane) * D + c);
+          }
+        }
+        cp_async_commit();
+      };
+      if (twarp == 0) {
+        issue(0);
+        issue(1);
+        cp_async_wait<1>();
+      }
+      named_bar(team_bar, TS);
+
+      for (int t = 0; t < ntiles; ++t) {
+        const int lr = (team + t * TEAMS) * TR;
+        const int rows = min(TR, nrows - lr);
+        const float* sl = S.slot[team][t & (kRing - 1)];
+        if (twarp == 0) issue(t + 2);   // slot (t+2)%4 was last read in tile t-2
+
+        // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero
+        // data); packed fp32x2 arithmetic (FFMA2/FADD2): two columns per instruction
+        float2 fr[TR][NV][2];
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          float x[D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) x[c] = sl[64 + i * 8 + c];
+          float al = 0.f;
+#pragma unroll
+          for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
+          al *= A.c2;
+          const float2 al2 = make_float2(al, al);
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            float2 e01 = add2(al2, make_float2(b2[j].x, b2[j].y));
+            float2 e23 = add2(al2, make_float2(b2[j].z, b2[j].w));
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const float2 xc = make_float2(x[c], x[c]);
+              e01 = fma2(make_float2(Wr[j][c].x, Wr[j][c].y), xc, e01);
+              e23 = fma2(make_float2(Wr[j][c].z, Wr[j][c].w), xc, e23);
+            }
+            fr[i][j][0] = make_float2(ex2(e01.x), ex2(e01.y));
+            fr[i][j][1] = make_float2(ex2(e23.x), ex2(e23.y));
+          }
+        }
+        const int rb = t & 1;
+        if constexpr (kDot) {
+          float pr[TR];
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            float2 pp = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              pp = fma2(fr[i][j][0], make_float2(s[j].x, s[j].y), pp);
+              pp = fma2(fr[i][j][1], make_float2(s[j].z, s[j].w), pp);
+            }
+            pr[i] = pp.x + pp.y;
+          }
+          const float tot = warp_transpose_reduce<TR>(pr, lane);
+          constexpr int kLanesPerRow = 32 / TR;
+          if ((lane & (kLanesPerRow - 1)) == 0) S.red[team][rb][twarp][lane / kLanesPerRow] = tot;
+        }
+        if (twarp == 0) cp_async_wait<1>();   // tile t+1 has landed (only t+2 may be pending)
+        named_bar(team_bar, TS);               // publishes red[rb] and slot (t+1) to the team
+
+        float vr_l = 0.f;
+        if constexpr (!kDot) {
+          vr_l = (lane < rows) ? 1.f : 0.f;   // u^0 = 1 (reading C6)
+        } else {
+          if (lane < rows) {
+            float tt = 0.f;
+#pragma unroll
+            for (int w = 0; w < NWT; ++w) tt += S.red[team][rb][w][lane];   // fixed order
+            const float c = sl[lane];
+            if constexpr (kAcc) vr_l = __fdiv_rn(c, tt);
+            if (twarp == NWT - 1) {   // the loader is warp 0: outputs go to the last warp
+              if (err_here) errsum += fabs((double)sl[32 + lane] * (double)tt - (double)c);
+              if constexpr (kOut) {
+                if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
+                outp0[lr + lane] = vr_l;
+              }
+            }
+          }
+        }
+        if constexpr (kAcc) {
+#pragma unroll
+          for (int i = 0; i < TR; ++i) {
+            const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+            const float2 v2 = make_float2(vi, vi);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              const float2 lo = fma2(fr[i][j][0], v2, make_float2(acc32[j].x, acc32[j].y));
+              const float2 hi = fma2(fr[i][j][1], v2, make_float2(acc32[j].z, acc32[j].w));
+              acc32[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
+            }
+          }
+          if ((t & (kFlushTiles - 1)) == kFlushTiles - 1) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+              acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
+              acc_s[j * 4 + 1][tid] += (double)acc32[j].y;
+              acc_s[j * 4 + 2][tid] += (double)acc32[j].z;
+              acc_s[j * 4 + 3][tid] += (double)acc32[j].w;
+              acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
         }
       }
-      cp_async_commit();
     };
-    if (twarp == 0) {
-      issue(0);
-      issue(1);
-      cp_async_wait<1>();
-    }
-    named_bar(team_bar, TS);
-
-    for (int t = 0; t < ntiles; ++t) {
-      const int64_t row0 = r0 + (int64_t)(team + t * TEAMS) * TR;
-      const int rows = (int)min((int64_t)TR, r1 - row0);
-      const float* sl = S.slot[team][t % kRing];
-      if (twarp == 0) issue(t + 2);   // slot (t+2)%4 was last read in tile t-2 (< previous barrier)
-
-      // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero data);
-      // packed fp32x2 arithmetic (FFMA2/FADD2): two columns per instruction
-      float2 fr[TR][NV][2];
-#pragma unroll
-      for (int i = 0; i < TR; ++i) {
-        float x[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) x[c] = sl[64 + i * 8 + c];
-        float al = 0.f;
-#pragma unroll
-        for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
-        al *= A.c2;
-        const float2 al2 = make_float2(al, al);
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          float2 e01 = add2(al2, make_float2(b2[j].x, b2[j].y));
-          float2 e23 = add2(al2, make_float2(b2[j].z, b2[j].w));
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            const float2 xc = make_float2(x[c], x[c]);
-            e01 = fma2(make_float2(Wr[j][c].x, Wr[j][c].y), xc, e01);
-            e23 = fma2(make_float2(Wr[j][c].z, Wr[j][c].w), xc, e23);
-          }
-          fr[i][j][0] = make_float2(ex2(e01.x), ex2(e01.y));
-          fr[i][j][1] = make_float2(ex2(e23.x), ex2(e23.y));
-        }
-      }
-      const int rb = t & 1;
-      if (kind != PK_INIT) {
-        float pr[TR];
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          float2 pp = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            pp = fma2(fr[i][j][0], make_float2(s[j].x, s[j].y), pp);
-            pp = fma2(fr[i][j][1], make_float2(s[j].z, s[j].w), pp);
-          }
-          pr[i] = pp.x + pp.y;
-        }
-        const float tot = warp_transpose_reduce<TR>(pr, lane);
-        constexpr int kLanesPerRow = 32 / TR;
-        if ((lane & (kLanesPerRow - 1)) == 0) S.red[team][rb][twarp][lane / kLanesPerRow] = tot;
-      }
-      if (twarp == 0) cp_async_wait<1>();   // tile t+1 has landed (only t+2 may be pending)
-      named_bar(team_bar, TS);               // publishes red[rb] and slot (t+1) to the team
-
-      float vr_l = 0.f;
-      if (kind == PK_INIT) {
-        vr_l = (lane < rows) ? 1.f : 0.f;   // u^0 = 1 (reading C6)
-      } else if (lane < rows) {
-        float tt = 0.f;
-#pragma unroll
-        for (int w = 0; w < NWT; ++w) tt += S.red[team][rb][w][lane];   // fixed order
-        const float c = sl[lane];
-        if (kind != PK_ERR) vr_l = __fdiv_rn(c, tt);
-        if (twarp == NWT - 1) {   // the loader is warp 0: outputs go to the last warp
-          if (kind == PK_ERR || (kind == PK_V && p >= 3))
-            errsum += fabs((double)sl[32 + lane] * (double)tt - (double)c);
-          if (kind != PK_ERR) {
-            if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
-            outp[row0 + lane] = vr_l;
-          }
-        }
-      }
-      if (kind != PK_ERR) {
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          const float vi = __shfl_sync(0xffffffffu, vr_l, i);
-          const float2 v2 = make_float2(vi, vi);
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            const float2 lo = fma2(fr[i][j][0], v2, make_float2(acc32[j].x, acc32[j].y));
-            const float2 hi = fma2(fr[i][j][1], v2, make_float2(acc32[j].z, acc32[j].w));
-            acc32[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
-          }
-        }
-        if (++tiles_since_flush == kFlushTiles) {
-          tiles_since_flush = 0;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
-            acc_s[j * 4 + 1][tid] += (double)acc32[j].y;
-            acc_s[j * 4 + 2][tid] += (double)acc32[j].z;
-            acc_s[j * 4 + 3][tid] += (double)acc32[j].w;
-            acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      }
+    switch (kind) {
+      case PK_INIT: run_tiles(std::integral_constant<int, PK_INIT>{}); break;
+      case PK_V: run_tiles(std::integral_constant<int, PK_V>{}); break;
+      case PK_U: run_tiles(std::integral_constant<int, PK_U>{}); break;
+      default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
     }
     if (twarp == 0) cp_async_wait<0>();
 #pragma unroll
