@@ -47,8 +47,8 @@ struct Smem {
   float red[3][NW][32];
   double xs[2][NW];
   double ext[kExtra];
-  int done_pass;
-  int stop;
+  int done_seq;   // last pass finished by the consumers: base(k) + pass, k-th problem of the CTA
+  int stop_seq;   // base(k) once the k-th problem of the CTA has stopped (tolerance mode)
 };
 
 template <bool IMPL, int NV, int TR, int D>
@@ -59,12 +59,14 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int prob = blockIdx.x / A.gpp;
-  const int cta = blockIdx.x - prob * A.gpp;
+  // groups of gpp CTAs; a group runs problems group, group + ngroups, ... (persistent)
+  const int group = blockIdx.x / A.gpp;
+  const int cta = blockIdx.x - group * A.gpp;
+  const int ngroups = (int)gridDim.x / A.gpp;
   const int r = A.r;
-  double* stg_state = A.state + (int64_t)prob * kStateDoubles;
+  const int seq_stride = A.num_passes + 2;
 
-  if (__ldcg(stg_state + ST_STOP) != 0.0) return;   // solve already finished (multi-launch)
+  if (A.multi_launch && __ldcg(A.state + ST_STOP) != 0.0) return;   // solve already finished
 
   if (tid == 0) {
     for (int i = 0; i < A.nstage; ++i) {
@@ -72,8 +74,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       mbar_init(&S.empty[i], NW);  // one arrival per consumer warp
     }
     for (int i = 0; i < 3; ++i) mbar_init(&S.redbar[i], NT);
-    S.done_pass = A.pass_begin - 1;
-    S.stop = 0;
+    S.done_seq = A.pass_begin - 1;
+    S.stop_seq = -1;
     fence_mbar_init();
   }
   // zero the ring once: tail tiles then compute on finite data without per-row predicates
@@ -87,6 +89,10 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     uint32_t stage = 0, phase = 0;
     const uint64_t pol = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
+    int pk = 0;
+    for (int prob = group; prob < A.nprob; prob += ngroups, ++pk) {
+    const int base = pk * seq_stride;
+    bool stopped_here = false;
     for (int p = A.pass_begin; p < A.pass_end; ++p) {
       const int kind = pass_kind(p, A);
       if (kind == PK_NONE) continue;
@@ -96,10 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (need_vold) wait_for = p - 2;                      // v_old written by pass p-2
       if (A.tol_mode && kind == PK_U && p >= 4) wait_for = p - 1;   // stop decision
       if (wait_for >= A.pass_begin) {
-        while (*(volatile int*)&S.done_pass < wait_for) __nanosleep(32);
+        while (*(volatile int*)&S.done_seq < base + wait_for) __nanosleep(32);
         __syncwarp();
         __threadfence_block();
-        if (*(volatile int*)&S.stop) break;
+        if (*(volatile int*)&S.stop_seq == base) {
+          stopped_here = true;
+          break;
+        }
       }
       int64_t r0, r1;
       cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
@@ -138,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         }
       }
     }
+    (void)stopped_here;
+    }   // problems
     return;
   }
 
@@ -178,17 +189,20 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     for (int q = 0; q < 4; ++q) acc64[j][q] = 0.0;
   }
 
+  uint32_t stage = 0, phase = 0;
+  uint32_t tk = 0;         // tiles that used a red buffer (buffer tk % 3, phase (tk / 3) & 1)
+  const bool multi = A.multi_launch != 0;
+  const int64_t rstride = r + kExtra;
+  int pk = 0;
+  for (int prob = group; prob < A.nprob; prob += ngroups, ++pk) {
+  const int base = pk * seq_stride;
+  double* stg_state = A.state + (int64_t)prob * kStateDoubles;
   // running solve state (identical in every CTA of the problem)
   double stErr = __ldcg(stg_state + ST_ERR);
   double stBrk = __ldcg(stg_state + ST_BRK);
-  const int64_t rstride = r + kExtra;
   double* part = A.part + (int64_t)prob * rstride * A.gpp;
   double* svec = A.svec + (int64_t)prob * rstride;
-  const bool multi = A.multi_launch != 0;
-  unsigned int nbar = 0;   // group barriers passed in this launch (counter zeroed per launch)
-
-  uint32_t stage = 0, phase = 0;
-  uint32_t tk = 0;         // tiles that used a red buffer (buffer tk % 3, phase (tk / 3) & 1)
+  unsigned int nbar = 0;   // group barriers passed for this problem in this launch
   int final_t = -1, conv = 0;
   double ferr = -1.0;
 
@@ -226,9 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
       }
       if (tid == 0) {
-        if (final_t >= 0) S.stop = 1;
+        if (final_t >= 0) *(volatile int*)&S.stop_seq = base;
         __threadfence_block();
-        *(volatile int*)&S.done_pass = q;
+        *(volatile int*)&S.done_seq = base + q;
       }
       if (final_t >= 0) break;
     }
@@ -577,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     stg_state[ST_ERR] = stErr;
     stg_state[ST_BRK] = stBrk;
   }
+  }   // problems
 }
 
 // ------------------------------------------------------------------------------------------
