@@ -200,7 +200,9 @@ def run_lsk(args):
     cfg = synth.get_config(args.config)
     variant = args.variant
     if variant == "auto":
-        variant = "stream"   # measured faster on configs 2-4
+        # measured: the MUFU-recompute variant is faster where it applies
+        # (d <= 8: configs 1, 2, 5); the factor stream elsewhere (configs 3, 4)
+        variant = "implicit" if cfg.d <= 8 else "stream"
     n_loc, m_loc = cfg.n, cfg.m
     # weak scaling: the global problem has ws x the per-GPU rows; each rank owns one shard
     full = synth.make_problem(cfg, n=cfg.n * ws, m=cfg.m * ws)
@@ -216,113 +218,124 @@ def run_lsk(args):
     U = torch.empty((r, d), dtype=torch.float32, device=dev)
     u = torch.empty(n_loc, dtype=torch.float32, device=dev)
     v = torch.empty(m_loc, dtype=torch.float32, device=dev)
-    Xi = Ze = None
-    if variant == "stream":
-        Xi = torch.empty((n_loc, r), dtype=torch.float32, device=dev)
-        Ze = torch.empty((m_loc, r), dtype=torch.float32, device=dev)
     opts = L.make_opts(T, 0.0, False, args.ctas_per_sm)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-
-    def step(ev_k0=None, ev_k1=None):
-        p = L.lsk_feature_params_init(eps, d, r, 0.0, cfg.anchor_seed, X, Y, comm=comm)
-        L.lsk_draw_anchors(p, U)
-        if variant == "stream":
-            L.lsk_feature_map(p, U, X, Xi)
-            L.lsk_feature_map(p, U, Y, Ze)
-            if ev_k0 is not None:
-                ev_k0.record(stream)
-            rep = L.lsk_factored_sinkhorn(Xi, Ze, a, b, eps, opts, u, v, report=False, comm=comm)
-        else:
-            if ev_k0 is not None:
-                ev_k0.record(stream)
-            rep = L.lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, report=False,
-                                                   comm=comm)
-        if ev_k1 is not None:
-            ev_k1.record(stream)
-        # read-out on the host (the step's result): fp64 ROT from the same call's state
-        return L.lsk_rot_value(u, v, a, b, eps, comm=comm)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    clocks = ClockSampler(local)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    L.launch_count(reset=True)
-    step_ms, kern_ms = [], []
-    rot_val = None
-    for _ in range(args.steps):
-        flush.zero_()                          # L2 flush, outside the timed events
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rot_val = step(k0, k1)
-        e1.record(stream)
-        e1.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-        kern_ms.append(k0.elapsed_time(k1))
-    launches = L.launch_count()
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    clk = clocks.stop()
-    tot_ms = float(np.sum(step_ms))
-    kmean = float(np.mean(kern_ms))
-    if dist is not None:
-        t = torch.tensor([tot_ms, kmean], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, kmean = float(t[0]), float(t[1])
-    ms_per_step = tot_ms / args.steps
-    units = ws                                  # config-sized problem-units per step
-    value = units * T * args.steps / (tot_ms / 1e3)
-
-    # roofline of the dominant kernel (the persistent Sinkhorn launch)
     peaks, src = _peaks()
-    sm_clock = (clk.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
-    if variant == "stream":
-        passes_rows = n_loc + T * (n_loc + m_loc)
-        alg_bytes = 4.0 * r * passes_rows + 8.0 * passes_rows + 4.0 * m_loc * (T - 1)
-        achieved = alg_bytes / (kmean / 1e3) / 1e9
-        peak = float(peaks["hbm_gbs"])
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % src,
-                "algorithmic_bytes_per_launch": alg_bytes}
-    else:
-        ex2 = float(r) * (n_loc + T * (n_loc + m_loc))
-        achieved = ex2 / (kmean / 1e3) / 1e9
-        peak = 4626.0   # measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gex2/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_source": "MUFU ex2 measured on B200 (profiles/r01_mufu_microbench.txt)",
-                "algorithmic_ex2_per_launch": ex2}
-    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            tr = json.load(open(tr_path)).get("config%d-%s" % (cfg.key, variant))
-            if tr:
-                roof["traffic"] = tr
-        except Exception:
-            pass
 
+    def measure(var, steps, warmup, sample_clocks):
+        Xi = Ze = None
+        if var == "stream":
+            Xi = torch.empty((n_loc, r), dtype=torch.float32, device=dev)
+            Ze = torch.empty((m_loc, r), dtype=torch.float32, device=dev)
+
+        def step(ev_k0=None, ev_k1=None):
+            p = L.lsk_feature_params_init(eps, d, r, 0.0, cfg.anchor_seed, X, Y, comm=comm)
+            L.lsk_draw_anchors(p, U)
+            if var == "stream":
+                L.lsk_feature_map(p, U, X, Xi)
+                L.lsk_feature_map(p, U, Y, Ze)
+                if ev_k0 is not None:
+                    ev_k0.record(stream)
+                L.lsk_factored_sinkhorn(Xi, Ze, a, b, eps, opts, u, v, report=False, comm=comm)
+            else:
+                if ev_k0 is not None:
+                    ev_k0.record(stream)
+                L.lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, report=False,
+                                                 comm=comm)
+            if ev_k1 is not None:
+                ev_k1.record(stream)
+            # read-out on the host (the step's result): fp64 ROT from the same call's state
+            return L.lsk_rot_value(u, v, a, b, eps, comm=comm)
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local) if sample_clocks else None
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        L.launch_count(reset=True)
+        step_ms, kern_ms = [], []
+        rot_val = None
+        for _ in range(steps):
+            flush.zero_()                          # L2 flush, outside the timed events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rot_val = step(k0, k1)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(k0.elapsed_time(k1))
+        launches = L.launch_count()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clk = clocks.stop() if clocks else None
+        tot_ms = float(np.sum(step_ms))
+        kmean = float(np.mean(kern_ms))
+        if dist is not None:
+            t = torch.tensor([tot_ms, kmean], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_ms, kmean = float(t[0]), float(t[1])
+        units = ws                                  # config-sized problem-units per step
+        value = units * T * steps / (tot_ms / 1e3)
+        # roofline of the dominant kernel (the persistent Sinkhorn launch)
+        if var == "stream":
+            passes_rows = n_loc + T * (n_loc + m_loc)
+            alg_bytes = 4.0 * r * passes_rows + 8.0 * passes_rows + 4.0 * m_loc * (T - 1)
+            achieved = alg_bytes / (kmean / 1e3) / 1e9
+            peak = float(peaks["hbm_gbs"])
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % src,
+                    "algorithmic_bytes_per_launch": alg_bytes}
+        else:
+            ex2 = float(r) * (n_loc + T * (n_loc + m_loc))
+            achieved = ex2 / (kmean / 1e3) / 1e9
+            peak = 4626.0   # measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gex2/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": "MUFU ex2 measured on B200 (profiles/r01_mufu_microbench.txt)",
+                    "algorithmic_ex2_per_launch": ex2}
+        tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tr_path):
+            try:
+                tr = json.load(open(tr_path)).get("config%d-%s" % (cfg.key, var))
+                if tr:
+                    roof["traffic"] = tr
+            except Exception:
+                pass
+        return {"value": value, "ms_per_step": tot_ms / steps, "kernel_ms": kmean,
+                "launches": int(launches), "clocks": clk, "rot": rot_val, "roofline": roof}
+
+    main_m = measure(variant, args.steps, args.warmup, True)
     result = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "metric": METRIC, "value": main_m["value"], "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_m["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
         "config": {"workload": "config%d-%s" % (cfg.key, cfg.name), "variant": variant,
                    "n_per_gpu": cfg.n, "m_per_gpu": cfg.m, "d": d, "r": r, "eps": eps, "T": T,
                    "global_n": cfg.n * ws, "parallelism": "rows%d" % ws if ws > 1 else "single",
                    "l2": "flushed (256 MiB write) before every timed step"},
-        "roofline": roof,
-        "kernel_ms": kmean,
-        "gpu_launches": int(launches),
-        "clocks": clk,
-        "rot": rot_val,
+        "roofline": main_m["roofline"],
+        "kernel_ms": main_m["kernel_ms"],
+        "gpu_launches": main_m["launches"],
+        "clocks": main_m["clocks"],
+        "rot": main_m["rot"],
     }
+    # the other variant on the same workload (same timing protocol), for the comparison the
+    # variant choice rests on; its roofline is the HBM one when it is the factor stream
+    if ws == 1 and not args.no_alt and cfg.d <= 8:
+        alt = "stream" if variant == "implicit" else "implicit"
+        m = measure(alt, args.steps, args.warmup, False)
+        result["alt_variant"] = {"variant": alt, "value": m["value"], "unit": UNIT,
+                                 "ms_per_step": m["ms_per_step"], "kernel_ms": m["kernel_ms"],
+                                 "roofline": m["roofline"], "rot": m["rot"]}
 
     # end-to-end through the public host-buffer entry point (N=1 only)
     if ws == 1 and not args.no_e2e:
@@ -372,6 +385,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other variant")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "lsk":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

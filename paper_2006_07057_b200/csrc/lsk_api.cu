@@ -182,16 +182,16 @@ struct SolveCfg {
 
 static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o, SolveCfg* c) {
   if (A.r > 4096) return fail(LSK_EDIM, "implicit variant supports r <= 4096");
-  int nt, nv, tr;
-  implicit_config(A.r, &nt, &nv, &tr);
-  A.tr = tr;
-  A.nv = nv;
+  const ImplCfg ic = implicit_config(A.r, A.d);
+  A.tr = ic.tr;
+  A.nv = ic.nv;
+  const int tr = ic.tr;
   c->impl = true;
   c->batch = batch;
   c->smem = 0;
   c->nstage = 0;
   c->stage_floats = 0;
-  int occ = implicit_max_ctas_per_sm(A.r, A.d);
+  int occ = implicit_max_ctas_per_sm(A);
   if (occ < 1) return fail(LSK_EUNSUPPORTED, "implicit kernel does not fit on an SM");
   int cps = (o && o->ctas_per_sm > 0) ? std::min(o->ctas_per_sm, occ) : occ;
   if (batch > 1) {
@@ -205,6 +205,26 @@ static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o,
     if (const char* e = getenv("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
     c->coop = c->gpp > 1;
+  }
+  return LSK_OK;
+}
+
+// Factored exponent of the implicit kernel (lsk_implicit.cu header): used when the row factor
+// h_j = 2^(alpha2_j - abar) stays within 2^{+-60}, i.e. (log2e/eps) R^2 <= 60.  LSK_FACT=0
+// forces the plain expanded form (tests cover both).
+static lsk_status setup_fact(SinkArgs& A, double R, int batch, cudaStream_t s, char* ws,
+                             Carve& cv) {
+  A.hrow[0] = A.hrow[1] = nullptr;
+  A.abar = 0.f;
+  const char* e = getenv("LSK_FACT");
+  if (e && atoi(e) == 0) return LSK_OK;
+  const double span = 1.4426950408889634074 / A.eps * R * R;
+  if (!(R > 0.0) || !(span <= 60.0)) return LSK_OK;
+  A.abar = (float)(-span);   // = c2 R^2 / 2, the middle of alpha2's range [c2 R^2, 0]
+  for (int f = 0; f < 2; ++f) {
+    float* h = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * A.rows[f] * batch));
+    LSK_CU(launch_row_scale(A.X[f], A.rows[f] * batch, A.d, A.c2, A.abar, h, s));
+    A.hrow[f] = h;
   }
   return LSK_OK;
 }
@@ -377,9 +397,10 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   return LSK_OK;
 }
 
-static size_t solve_ws_bytes(int r, int64_t m, int batch, int gpp_max) {
+static size_t solve_ws_bytes(int r, int64_t m, int batch, int gpp_max, int64_t n = 0) {
   const int64_t rs = r + kExtra;
-  return 256 * 8 + sizeof(double) * rs * gpp_max * batch + sizeof(double) * rs * batch +
+  return 256 * 8 + sizeof(float) * (n + m + 64) * batch +   // implicit row factors h (FACT)
+          sizeof(double) * rs * gpp_max * batch + sizeof(double) * rs * batch +
          sizeof(double) * kStateDoubles * batch + sizeof(unsigned) * batch +
          sizeof(float) * m * batch;
 }
@@ -587,7 +608,7 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
-  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms()), &ws));
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms(), n), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
@@ -599,6 +620,7 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   A.r = p->r; A.d = p->d; A.eps = p->eps;
   A.Wt = Wt; A.beta2 = b2;
   A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
+  LSK_TRY(setup_fact(A, p->R, 1, s, ws, cv));
   return run_solve(A, true, 1, o, rep, comm, s, ws, cv);
 }
 
@@ -673,7 +695,7 @@ lsk_status lsk_rot_value_batched(const float* u, const float* v, const float* a,
 static lsk_status divergence_impl(bool impl, const float* F, int64_t n, const float* G,
                                   int64_t m, int r, int d, const float* a, const float* b,
                                   double eps, const float* Wt, const float* b2, float c2,
-                                  const lsk_solve_opts* o, double* out4, lsk_report* reps3,
+                                  double R, const lsk_solve_opts* o, double* out4, lsk_report* reps3,
                                   cudaStream_t s, char* ws, Carve& cv) {
   const int64_t mx = std::max(n, m);
   float* us = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * mx));
@@ -692,6 +714,7 @@ static lsk_status divergence_impl(bool impl, const float* F, int64_t n, const fl
     A.r = r; A.d = d; A.eps = eps;
     A.Wt = Wt; A.beta2 = b2; A.c2 = c2;
     Carve cv2 = cv;   // each solve reuses the same workspace tail
+    if (impl) LSK_TRY(setup_fact(A, R, 1, s, ws, cv2));
     lsk_report rep{};
     lsk_status st = run_solve(A, impl, 1, o, &rep, nullptr, s, ws, cv2);
     if (st < 0) return st;
@@ -787,7 +810,7 @@ lsk_status lsk_sinkhorn_divergence(const float* Xi, int64_t n, const float* Zeta
   char* ws;
   LSK_TRY(get_ws(s, 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(r, mx, 1, 2 * num_sms()), &ws));
   Carve cv;
-  return divergence_impl(false, Xi, n, Zeta, m, r, 1, a, b, eps, nullptr, nullptr, 0.f, o,
+  return divergence_impl(false, Xi, n, Zeta, m, r, 1, a, b, eps, nullptr, nullptr, 0.f, 0.0, o,
                          out4_host, reps3, s, ws, cv);
 }
 
@@ -806,12 +829,12 @@ lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const f
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
-  LSK_TRY(get_ws(s, cv.off + 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(p->r, mx, 1, 2 * num_sms()), &ws));
+  LSK_TRY(get_ws(s, cv.off + 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(p->r, mx, 1, 2 * num_sms(), mx), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
   return divergence_impl(true, X, n, Y, m, p->r, p->d, a, b, p->eps, Wt, b2,
-                         (float)(-2.0 * 1.4426950408889634074 / p->eps), o, out4_host, reps3, s,
+                         (float)(-2.0 * 1.4426950408889634074 / p->eps), p->R, o, out4_host, reps3, s,
                          ws, cv);
 }
 

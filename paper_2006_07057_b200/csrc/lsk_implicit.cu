@@ -3,19 +3,34 @@
 // point rows and the anchors (Lemma decomp-RBF, expanded in base 2):
 //     F_jk = 2^( alpha2_j + beta2_k + sum_c W_kc p_jc ),
 //     alpha2_j = -(2 log2e/eps)|p_j|^2, W_kc = (4 log2e/eps) U_kc,
-//     beta2_k = log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
-// so a pass costs one MUFU ex2 + (d+3) FFMA-pipe ops per entry and ~(4d+12) bytes per row.
+//     beta2_k = log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale).
 //
-// Layout: one CTA per SM made of TEAMS independent teams of TS threads (all consumers, no
-// producer warp: 512 threads x 128 registers).  A team owns every column: thread t of a
-// team owns float4 column groups {t, t+TS, ...} (its W, beta2, slice of s and accumulators
-// live in registers).  The teams take alternate tiles of the CTA's rows, each with its own
-// loader warp (cp.async two tiles ahead into a 4-slot ring) and its own named barrier, so
-// while one team waits on its per-tile row-dot exchange the other team issues MUFU work.
-// The two teams' fp64 partials are added in a fixed order at the end of the pass.  Pass
-// boundary, stopping test and the fp64 read-out are those of the streaming kernel.
+// Factored exponent (FACT, DESIGN.md §6 K5): the row term is pulled out of the entry,
+//     F_jk = h_j G_jk,  G_jk = 2^(beta2_k + abar + sum_c W_kc p_jc),  h_j = 2^(alpha2_j - abar),
+// with abar = -(log2e/eps) R^2 (mid-range of alpha2, so h_j is within 2^{+-(log2e/eps)R^2}).
+// Then t_j = h_j (G_j . s), w_j = c_j / t_j, and the accumulation s'_k = sum_j F_jk w_j =
+// sum_j G_jk (h_j w_j): per entry only the d-term dot W_k . p_j and one MUFU ex2 remain
+// (d FFMA2 per column pair instead of d+1, and no per-entry |p|^2 work).  The host uses it
+// when (log2e/eps) R^2 <= 60 (G, h stay far from the fp32 range limits); otherwise the plain
+// expanded form (h = 1, abar folded per row) runs.
+//
+// Layout: one CTA per SM made of TEAMS teams of TS threads (all consumers).  A team owns every
+// column: thread t of a team owns float4 column groups {t, t+TS, ...} (its W, beta2, slice of
+// s and fp32 accumulators live in registers; the fp64 accumulators in shared memory).  Teams
+// take alternate tiles of TR rows of the CTA's row range.  Each team's warp 0 stages tiles
+// (point rows, c_j, h_j, v_old_j) kAhead tiles ahead with cp.async into an 8-slot ring whose
+// completion is tracked on per-slot mbarriers.
+//
+// Software pipeline (per team, lag one tile): tile t's features are generated and its row-dot
+// partials published (red[t%3], split mbarrier arrive) BEFORE tile t-1 is finished (wait,
+// scalings, accumulation), so the cross-warp exchange latency of one tile overlaps the MUFU
+// work of the next.  The exchange is spread over lanes: row i's NWT warp partials are summed
+// by G lanes (NWT/G each) and a fixed xor butterfly — every lane of the group ends with the
+// same bits, and the order never changes (deterministic).  Pass boundary, stopping test and
+// the fp64 read-out are those of the streaming kernel (lsk_sinkhorn.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -27,62 +42,96 @@ namespace lsk {
 
 namespace impl {
 
-constexpr int kRing = 4;            // tile slots (two tiles in flight ahead of the current)
-constexpr int kSlot = 64 + 32 * 8;  // floats per slot: c[32], vold[32], x[32][8]
+constexpr int kRing = 16;   // tile slots per team
+constexpr int kAhead = 8;   // the loader stages tile t+kAhead when tile t starts (<= kRing/2)
 
-template <int TS, int TEAMS>
-struct Smem {
-  float slot[TEAMS][kRing][kSlot];
-  float red[TEAMS][2][TS / 32][32];
-  double xs[2][TS * TEAMS / 32];
-  double ext[kExtra];
+template <int D>
+struct Geo {
+  static constexpr int XS = D <= 4 ? 4 : 8;        // floats per staged point row
+  static constexpr int SLOT = 96 + 32 * XS;        // c[32] h[32] vold[32] x[32][XS]
 };
 
-template <int TS, int TEAMS, int NV, int TR, int D>
+template <int TS, int TEAMS, int TR>
+struct Smem {
+  uint64_t full[TEAMS][kRing];     // slot landed (32 cp.async arrivals of the loader warp)
+  uint64_t redbar[TEAMS][3];       // row-dot partials of a tile published (TS arrivals)
+  float red[TEAMS][3][TR][TS / 32];
+  double xs[2][TS * TEAMS / 32];
+  double ext[kExtra];
+  double errL[TEAMS][32];          // per-lane marginal-error sums of the output warps
+  double brkL[TEAMS][32];          // per-lane breakdown counts of the output warps
+  double st[3];                    // running solve state: err, breakdowns, final err
+  int ist[2];                      // final_t, conv
+};
+
+template <int TS, int TEAMS, int NV, int TR, int D, bool FACT, bool PIPE>
 __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs A) {
   constexpr int NT = TS * TEAMS;       // CTA threads
   constexpr int NWT = TS / 32;         // warps per team
   constexpr int NW = NT / 32;
-  constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;
-  static_assert(TEAMS == 1 || TEAMS == 2 || TEAMS == 4, "1, 2 or 4 teams");
-  __shared__ __align__(16) Smem<TS, TEAMS> S;
-  // fp64 accumulators of every thread in shared memory (touched once per kFlushTiles tiles):
-  // element-major so consecutive threads hit consecutive words
-  extern __shared__ double acc_dyn[];   // dynamic: [NV * 4][NT]
+  constexpr int XS = Geo<D>::XS, SLOT = Geo<D>::SLOT;
+  constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;   // fp32 partial over <= 32 rows
+  constexpr int LPR = 32 / TR;                                   // lanes per row after the transpose-reduce
+  constexpr int G = NWT < LPR ? NWT : LPR;                       // lanes per row in the exchange
+  constexpr int PER = NWT / G;                                   // partials summed per lane
+  static_assert(TEAMS >= 1 && TEAMS <= 4, "1 to 4 teams");
+  static_assert(TR * G <= 32 && NWT % G == 0, "exchange layout");
+  __shared__ __align__(16) Smem<TS, TEAMS, TR> S;
+  // dynamic: fp64 accumulators [NV*4][NT] (element-major: consecutive threads, consecutive
+  // words), then the tile slots [TEAMS][kRing][SLOT]
+  extern __shared__ double acc_dyn[];
   double (*acc_s)[NT] = reinterpret_cast<double (*)[NT]>(acc_dyn);
+  float* slots = reinterpret_cast<float*>(acc_dyn + NV * 4 * NT);
+  float4* s_sm = reinterpret_cast<float4*>(slots + TEAMS * kRing * SLOT);   // [NV * TS] s in fp32
 
   const int tid = threadIdx.x;
   const int team = tid / TS, ttid = tid - team * TS;
   const int warp = tid >> 5, lane = tid & 31;
   const int twarp = ttid >> 5;          // warp index within the team
-  const uint32_t team_bar = 2u + (uint32_t)team;   // ids 2..5 (1 = whole CTA)
+  const uint32_t team_bar = 2u + (uint32_t)team;   // named barrier ids 2..5 (1 = whole CTA)
   const int prob = blockIdx.x / A.gpp;
   const int cta = blockIdx.x - prob * A.gpp;
   const int r = A.r;
   double* stg_state = A.state + (int64_t)prob * kStateDoubles;
   if (__ldcg(stg_state + ST_STOP) != 0.0) return;   // finished (multi-launch mode)
 
-  // per-thread anchor constants for the owned column groups
+  if (tid == 0) {
+    for (int tm = 0; tm < TEAMS; ++tm) {
+      for (int i = 0; i < kRing; ++i) mbar_init(&S.full[tm][i], 32);
+      for (int i = 0; i < 3; ++i) mbar_init(&S.redbar[tm][i], TS);
+    }
+    fence_mbar_init();
+  }
+  // zero the slots once: tail rows then compute on finite data without per-row predicates
+  for (int i = tid; i < TEAMS * kRing * SLOT; i += NT) slots[i] = 0.f;
+
+  // per-thread anchor constants for the owned column groups (as float pairs for FFMA2)
   const int R4 = r >> 2;
   int g[NV];
   bool gv[NV];
-  float4 Wr[NV][D];
-  float4 b2[NV];
+  float2 W2[NV][D][2];
+  float2 B2[NV][2];
+  const float boff = FACT ? A.abar : 0.f;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     g[j] = ttid + j * TS;
     gv[j] = g[j] < R4;
     if (gv[j]) {
-      b2[j] = *reinterpret_cast<const float4*>(A.beta2 + 4 * g[j]);
+      const float4 b = *reinterpret_cast<const float4*>(A.beta2 + 4 * g[j]);
+      B2[j][0] = make_float2(b.x + boff, b.y + boff);
+      B2[j][1] = make_float2(b.z + boff, b.w + boff);
 #pragma unroll
-      for (int c = 0; c < D; ++c) Wr[j][c] = *reinterpret_cast<const float4*>(A.Wt + (int64_t)c * r + 4 * g[j]);
+      for (int c = 0; c < D; ++c) {
+        const float4 w = *reinterpret_cast<const float4*>(A.Wt + (int64_t)c * r + 4 * g[j]);
+        W2[j][c][0] = make_float2(w.x, w.y);
+        W2[j][c][1] = make_float2(w.z, w.w);
+      }
     } else {   // padding groups produce exact zeros: ex2(-inf) = 0
-      b2[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      B2[j][0] = B2[j][1] = make_float2(-INFINITY, -INFINITY);
 #pragma unroll
-      for (int c = 0; c < D; ++c) Wr[j][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < D; ++c) W2[j][c][0] = W2[j][c][1] = make_float2(0.f, 0.f);
     }
   }
-  for (int i = tid; i < TEAMS * kRing * kSlot; i += NT) (&S.slot[0][0][0])[i] = 0.f;
   __syncthreads();
 
   float4 s[NV];
@@ -93,49 +142,68 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     for (int q = 0; q < 4; ++q) acc_s[j * 4 + q][tid] = 0.0;
   }
 
-  double stErr = __ldcg(stg_state + ST_ERR);
-  double stBrk = __ldcg(stg_state + ST_BRK);
+  // running solve state in shared memory (uniform; keeps registers for the tile loop)
+  double& stErr = S.st[0];
+  double& stBrk = S.st[1];
+  double& ferr = S.st[2];
+  int& final_t = S.ist[0];
+  int& conv = S.ist[1];
+  if (tid == 0) {
+    stErr = __ldcg(stg_state + ST_ERR);
+    stBrk = __ldcg(stg_state + ST_BRK);
+    ferr = -1.0;
+    final_t = -1;
+    conv = 0;
+  }
+  if (tid < 32) {
+    for (int tm = 0; tm < TEAMS; ++tm) S.errL[tm][tid] = S.brkL[tm][tid] = 0.0;
+  }
+  __syncthreads();
   const int64_t rstride = r + kExtra;
   double* part = A.part + (int64_t)prob * rstride * A.gpp;
   double* svec = A.svec + (int64_t)prob * rstride;
   const bool multi = A.multi_launch != 0;
   unsigned int nbar = 0;
-  int final_t = -1, conv = 0;
-  double ferr = -1.0;
+  uint32_t gt = 0;   // tiles of this team so far in this launch: slot gt % kRing, red gt % 3
+
+  float* tslots = slots + team * kRing * SLOT;
 
   for (int p = A.pass_begin;; ++p) {
     // ---------------- results of pass q = p-1: stopping test (see lsk_sinkhorn.cu) -------
     const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
     if (have_prev) {
-      const int q = p - 1;
-      const int qk = pass_kind(q, A);
-      double e_err, e_brk;
-      if (A.gpp > 1) {
-        e_err = __ldcg(svec + r);
-        e_brk = __ldcg(svec + r + 1);
-      } else {
-        e_err = S.ext[0];
-        e_brk = S.ext[1];
-      }
-      stBrk += e_brk;
-      if (qk == PK_V) {
-        const int t = (q + 1) / 2;
-        if (t >= 2) {
-          stErr = e_err;
-          if (A.tol_mode && e_err < A.tol) {
-            final_t = t - 1;
-            ferr = e_err;
-            conv = 1;
-          }
+      if (tid == 0) {
+        const int q = p - 1;
+        const int qk = pass_kind(q, A);
+        double e_err, e_brk;
+        if (A.gpp > 1) {
+          e_err = __ldcg(svec + r);
+          e_brk = __ldcg(svec + r + 1);
+        } else {
+          e_err = S.ext[0];
+          e_brk = S.ext[1];
         }
-      } else if (qk == PK_ERR) {
-        stErr = e_err;
+        stBrk += e_brk;
+        if (qk == PK_V) {
+          const int t = (q + 1) / 2;
+          if (t >= 2) {
+            stErr = e_err;
+            if (A.tol_mode && e_err < A.tol) {
+              final_t = t - 1;
+              ferr = e_err;
+              conv = 1;
+            }
+          }
+        } else if (qk == PK_ERR) {
+          stErr = e_err;
+        }
+        if (final_t < 0 && q == A.num_passes - 1) {
+          final_t = A.T;
+          ferr = A.want_err ? stErr : -1.0;
+          conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
+        }
       }
-      if (final_t < 0 && q == A.num_passes - 1) {
-        final_t = A.T;
-        ferr = A.want_err ? stErr : -1.0;
-        conv = A.tol_mode ? (stErr < A.tol ? 1 : 0) : 0;
-      }
+      named_bar(1, NT);
       if (final_t >= 0) break;
     }
     if (p >= A.pass_end) break;
@@ -145,20 +213,25 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     if (kind == PK_NONE) continue;
     const int f = (kind == PK_V || kind == PK_ERR) ? 1 : 0;
     if (kind != PK_INIT) {
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        if (!gv[j]) {
-          s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else if (A.gpp > 1) {
-          const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j]));
-          const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j] + 2));
-          s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
-        } else {   // gpp == 1: the combined accumulator sits in team 0's slots
-          s[j] = make_float4((float)acc_s[j * 4][ttid], (float)acc_s[j * 4 + 1][ttid],
-                             (float)acc_s[j * 4 + 2][ttid], (float)acc_s[j * 4 + 3][ttid]);
+      // s -> fp32 in shared memory once per CTA (the teams share it; see lsk_implicit_warp.cu)
+      for (int gg = tid; gg < NV * TS; gg += NT) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gg < R4) {
+          if (A.gpp > 1) {
+            const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * gg));
+            const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * gg + 2));
+            v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+          } else {   // gpp == 1: the combined accumulator sits in team 0's slots
+            const int t0 = gg % TS, j = gg / TS;
+            v = make_float4((float)acc_s[j * 4][t0], (float)acc_s[j * 4 + 1][t0],
+                            (float)acc_s[j * 4 + 2][t0], (float)acc_s[j * 4 + 3][t0]);
+          }
         }
+        s_sm[gg] = v;
       }
-      named_bar(1, NT);   // every team has read team 0's slots before they are cleared
+      named_bar(1, NT);   // s staged; every team is done with team 0's slots
+#pragma unroll
+      for (int j = 0; j < NV; ++j) s[j] = s_sm[g[j]];
     }
 #pragma unroll
     for (int j = 0; j < NV; ++j)
@@ -167,90 +240,98 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 
     int64_t r0, r1;
     cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
-    const int ntiles_cta = (int)((r1 - r0 + TR - 1) / TR);
+    const int nrows = (int)(r1 - r0);
+    const int ntiles_cta = (nrows + TR - 1) / TR;
     const int ntiles = (ntiles_cta - team + TEAMS - 1) / TEAMS;   // this team: tiles team, team+TEAMS, ...
-    const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
-    const float* Xp = A.X[f] + (int64_t)prob * A.fstride[f];
+    const float* wp0 = A.w[f] + (int64_t)prob * A.wstride[f] + r0;
+    const float* Xp0 = A.X[f] + (int64_t)prob * A.fstride[f] + r0 * D;
+    const float* hp0 = FACT ? A.hrow[f] + (int64_t)prob * A.wstride[f] + r0 : nullptr;
     const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
-    const bool err_here = need_vold;
-    const float* vold = need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) : nullptr;
-    float* outp = nullptr;
-    if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
-    if (kind == PK_V) outp = vbuf_ptr(A, prob, (p + 1) / 2);
-    double errsum = 0.0, brksum = 0.0;
+    const float* vold0 =
+        need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) + r0 : nullptr;
+    float* outp0 = nullptr;
+    if (kind == PK_U) outp0 = A.out[0] + (int64_t)prob * A.wstride[0] + r0;
+    if (kind == PK_V) outp0 = vbuf_ptr(A, prob, (p + 1) / 2) + r0;
     float4 acc32[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint32_t gt0 = gt;
 
     // The tile loop is instantiated per pass kind (compile-time KIND: no per-tile kind
     // branches) with 32-bit row offsets relative to this CTA's first row.
-    const int nrows = (int)(r1 - r0);
-    const float* wp0 = wp + r0;
-    const float* vold0 = need_vold ? vold + r0 : nullptr;
-    const float* Xp0 = Xp + r0 * D;
-    float* outp0 = outp ? outp + r0 : nullptr;
-
     auto run_tiles = [&](auto kind_tag) {
       constexpr int KIND = decltype(kind_tag)::value;
       constexpr bool kDot = KIND != PK_INIT;
       constexpr bool kAcc = KIND != PK_ERR;
       constexpr bool kOut = KIND == PK_U || KIND == PK_V;
-      // warp 0 stages tile t (point rows + c_j + v_old_j) into slot t % kRing.  v_old_j was
-      // written by this same lane two passes earlier (same tiling), so no extra ordering.
+      // loader (team warp 0): tile t -> slot (gt0+t) % kRing.  v_old_j was written two passes
+      // earlier by this CTA (same rows, same tiling), so plain cp.async ordering suffices.
+      // PIPE: completion on the slot's mbarrier; !PIPE: one cp.async group per tile (empty ones
+      // too), waited by the loader before the team's per-tile named barrier publishes the slot
       auto issue = [&](int t) {
-        if (t < ntiles) {
-          const int lr = (team + t * TEAMS) * TR;
-          float* sl = S.slot[team][t & (kRing - 1)];
-          if (lane < nrows - lr && lane < TR) {
-            cp_async4(sl + lane, wp0 + lr + lane);
-            if (need_vold) cp_async4(sl + 32 + lane, vold0 + lr + lane);
-#pragma unroll
-            for (int c = 0; c < D; ++c) cp_async4(sl + 64 + lane * 8 + c, Xp0 + (lr + lane) * D + c);
-          }
+        if (t >= ntiles) {
+          if constexpr (!PIPE) cp_async_commit();
+          return;
         }
-        cp_async_commit();
+        const int lr = (team + t * TEAMS) * TR;
+        const uint32_t gi = gt0 + (uint32_t)t;
+        float* sl = tslots + (gi % kRing) * SLOT;
+        if (lane < TR && lane < nrows - lr) {
+          cp_async4(sl + lane, wp0 + lr + lane);
+          if (FACT) cp_async4(sl + 32 + lane, hp0 + lr + lane);
+          if (need_vold) cp_async4(sl + 64 + lane, vold0 + lr + lane);
+#pragma unroll
+          for (int c = 0; c < D; ++c) cp_async4(sl + 96 + lane * XS + c, Xp0 + (lr + lane) * D + c);
+        }
+        if constexpr (PIPE) cp_async_mbar_arrive_noinc(&S.full[team][gi % kRing]);
+        else cp_async_commit();
       };
       if (twarp == 0) {
-        issue(0);
-        issue(1);
-        cp_async_wait<1>();
+#pragma unroll
+        for (int t = 0; t < kAhead; ++t) issue(t);
+        if constexpr (!PIPE) cp_async_wait<kAhead - 1>();   // tile 0 landed
       }
-      named_bar(team_bar, TS);
+      if constexpr (!PIPE) named_bar(team_bar, TS);
 
-      for (int t = 0; t < ntiles; ++t) {
-        const int lr = (team + t * TEAMS) * TR;
-        const int rows = min(TR, nrows - lr);
-        const float* sl = S.slot[team][t & (kRing - 1)];
-        if (twarp == 0) issue(t + 2);   // slot (t+2)%4 was last read in tile t-2
-
-        // regenerate the TR x 4NV features of this thread (tail rows: finite stale/zero
-        // data); packed fp32x2 arithmetic (FFMA2/FADD2): two columns per instruction
-        float2 fr[TR][NV][2];
+      // generate tile t's features into fr and publish its row-dot partials
+      auto compute = [&](int t, float2 (&fr)[TR][NV][2]) {
+        if (twarp == 0) issue(t + kAhead);
+        const uint32_t gi = gt0 + (uint32_t)t;
+        const float* sl = tslots + (gi % kRing) * SLOT;
+        if constexpr (PIPE) mbar_wait(&S.full[team][gi % kRing], (gi / kRing) & 1u);
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
-          float x[D];
+          float x[XS];
+          {
+            const float4 x0 = lds128(sl + 96 + i * XS);
+            x[0] = x0.x; if (XS > 1) x[1] = x0.y;
+            if (XS > 2) x[2] = x0.z;
+            if (XS > 3) x[3] = x0.w;
+            if constexpr (XS > 4) {
+              const float4 x1 = lds128(sl + 96 + i * XS + 4);
+              x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
+            }
+          }
+          float2 al2 = make_float2(0.f, 0.f);
+          if constexpr (!FACT) {
+            float al = 0.f;
 #pragma unroll
-          for (int c = 0; c < D; ++c) x[c] = sl[64 + i * 8 + c];
-          float al = 0.f;
-#pragma unroll
-          for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
-          al *= A.c2;
-          const float2 al2 = make_float2(al, al);
+            for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
+            al *= A.c2;
+            al2 = make_float2(al, al);
+          }
 #pragma unroll
           for (int j = 0; j < NV; ++j) {
-            float2 e01 = add2(al2, make_float2(b2[j].x, b2[j].y));
-            float2 e23 = add2(al2, make_float2(b2[j].z, b2[j].w));
 #pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const float2 xc = make_float2(x[c], x[c]);
-              e01 = fma2(make_float2(Wr[j][c].x, Wr[j][c].y), xc, e01);
-              e23 = fma2(make_float2(Wr[j][c].z, Wr[j][c].w), xc, e23);
+            for (int h = 0; h < 2; ++h) {
+              float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);
+#pragma unroll
+              for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
+              fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
             }
-            fr[i][j][0] = make_float2(ex2(e01.x), ex2(e01.y));
-            fr[i][j][1] = make_float2(ex2(e23.x), ex2(e23.y));
           }
         }
-        const int rb = t & 1;
+        const int rb = (int)(gi % 3u);
         if constexpr (kDot) {
           float pr[TR];
 #pragma unroll
@@ -264,35 +345,60 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
             pr[i] = pp.x + pp.y;
           }
           const float tot = warp_transpose_reduce<TR>(pr, lane);
-          constexpr int kLanesPerRow = 32 / TR;
-          if ((lane & (kLanesPerRow - 1)) == 0) S.red[team][rb][twarp][lane / kLanesPerRow] = tot;
+          if ((lane & (LPR - 1)) == 0) S.red[team][rb][lane / LPR][twarp] = tot;
         }
-        if (twarp == 0) cp_async_wait<1>();   // tile t+1 has landed (only t+2 may be pending)
-        named_bar(team_bar, TS);               // publishes red[rb] and slot (t+1) to the team
-
-        float vr_l = 0.f;
-        if constexpr (!kDot) {
-          vr_l = (lane < rows) ? 1.f : 0.f;   // u^0 = 1 (reading C6)
+        if constexpr (PIPE) {
+          mbar_arrive(&S.redbar[team][rb]);   // also the per-tile team sync of the init pass
         } else {
-          if (lane < rows) {
-            float tt = 0.f;
+          if (twarp == 0) cp_async_wait<kAhead - 1>();   // tile t+1 landed
+          named_bar(team_bar, TS);   // publishes red[rb] and slot t+1 to the team
+        }
+      };
+
+      // finish tile t: wait for the team's partials, derive the TR scalings (every warp the
+      // same bits), write them (last warp), accumulate G^T w~ (w~ = h w)
+      int nfin = 0;
+      auto finish = [&](int t, float2 (&fr)[TR][NV][2]) {
+        const uint32_t gi = gt0 + (uint32_t)t;
+        const int lr = (team + t * TEAMS) * TR;
+        const int rows = min(TR, nrows - lr);
+        const float* sl = tslots + (gi % kRing) * SLOT;
+        const int rb = (int)(gi % 3u);
+        if constexpr (PIPE) mbar_wait(&S.redbar[team][rb], (gi / 3u) & 1u);
+        const int row = lane / G;
+        const bool valid = (lane < TR * G) && (row < rows);
+        float wt = 0.f;
+        if constexpr (kDot) {
+          float tot = 0.f;
+          if (lane < TR * G) {
+            const float* rp = &S.red[team][rb][row][(lane % G) * PER];
 #pragma unroll
-            for (int w = 0; w < NWT; ++w) tt += S.red[team][rb][w][lane];   // fixed order
-            const float c = sl[lane];
-            if constexpr (kAcc) vr_l = __fdiv_rn(c, tt);
-            if (twarp == NWT - 1) {   // the loader is warp 0: outputs go to the last warp
-              if (err_here) errsum += fabs((double)sl[32 + lane] * (double)tt - (double)c);
+            for (int q = 0; q < PER; ++q) tot += rp[q];
+          }
+#pragma unroll
+          for (int off = 1; off < G; off <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+          if (valid) {
+            const float c = sl[row];
+            const float h = FACT ? sl[32 + row] : 1.f;
+            const float tj = FACT ? h * tot : tot;     // t_j = F_j . s
+            const float w = c * rcp_approx(tj);        // w_j = c_j / t_j
+            wt = FACT ? w * h : w;
+            if (twarp == NWT - 1 && (lane % G) == 0) {   // outputs: one lane per row
+              if (need_vold) S.errL[team][lane] += fabs((double)sl[64 + row] * (double)tj - (double)c);
               if constexpr (kOut) {
-                if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
-                outp0[lr + lane] = vr_l;
+                if (!(w > 0.f) || !isfinite(w)) S.brkL[team][lane] += 1.0;
+                outp0[lr + row] = w;
               }
             }
           }
+          if constexpr (!kAcc) wt = 0.f;
+        } else {
+          if (valid) wt = FACT ? sl[32 + row] : 1.f;   // u^0 = 1 (reading C6): w~ = h
         }
         if constexpr (kAcc) {
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
-            const float vi = __shfl_sync(0xffffffffu, vr_l, i);
+            const float vi = __shfl_sync(0xffffffffu, wt, i * G);
             const float2 v2 = make_float2(vi, vi);
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
@@ -301,7 +407,8 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
               acc32[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
             }
           }
-          if ((t & (kFlushTiles - 1)) == kFlushTiles - 1) {
+          if (++nfin == kFlushTiles) {
+            nfin = 0;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
               acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
@@ -312,6 +419,30 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
             }
           }
         }
+      };
+
+      float2 frA[TR][NV][2];
+      if constexpr (PIPE) {
+        float2 frB[TR][NV][2];
+        if (ntiles > 0) {
+          int t = 0;
+          compute(0, frA);
+          while (true) {   // frA holds tile t
+            if (t + 1 >= ntiles) { finish(t, frA); break; }
+            compute(t + 1, frB);
+            finish(t, frA);
+            ++t;           // frB holds tile t
+            if (t + 1 >= ntiles) { finish(t, frB); break; }
+            compute(t + 1, frA);
+            finish(t, frB);
+            ++t;
+          }
+        }
+      } else {
+        for (int t = 0; t < ntiles; ++t) {
+          compute(t, frA);
+          finish(t, frA);
+        }
       }
     };
     switch (kind) {
@@ -320,7 +451,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       case PK_U: run_tiles(std::integral_constant<int, PK_U>{}); break;
       default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
     }
-    if (twarp == 0) cp_async_wait<0>();
+    gt += (uint32_t)((ntiles_cta - team + TEAMS - 1) / TEAMS);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
@@ -332,8 +463,10 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     // ---------------- end of pass: teams combined (fixed order), cross-CTA fp64 reduction ---
     double e0 = 0.0, e1 = 0.0;
     if (twarp == NWT - 1) {
-      e0 = warp_sum_f64(errsum);
-      e1 = warp_sum_f64(brksum);
+      e0 = warp_sum_f64(S.errL[team][lane]);
+      e1 = warp_sum_f64(S.brkL[team][lane]);
+      S.errL[team][lane] = 0.0;
+      S.brkL[team][lane] = 0.0;
     }
     if (twarp == NWT - 1 && lane == 0) {   // hand the team's extras to its thread 0
       S.xs[0][NW - 1 - team] = e0;
@@ -468,71 +601,138 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   }
 }
 
-}  // namespace impl
-
-// (TS, TEAMS, NV, TR) per r: r <= 1024 -> (256, 2, 1, 8); r <= 2048 -> (512, 1, 1, 8);
-// r <= 4096 -> (512, 1, 2, 2).  Always 512 threads, one CTA per SM.
-void implicit_config(int r, int* nt, int* nv, int* tr) {
-  const int r4 = (r + 3) / 4;
-  if (r4 <= 256) {
-    // four 128-thread teams, 8 columns per thread (halves the per-entry exchange overhead)
-    *nt = 128; *nv = 2; *tr = 4;
-    if (const char* e = getenv("LSK_ITEAM")) {   // tuning knob: 2 = two 256-thread teams
-      if (atoi(e) == 2) { *nt = 256; *nv = 1; *tr = 8; }
-    }
+// h_j = 2^(c2 |p_j|^2 - abar): the row factor of the factored exponent (same fp32 arithmetic
+// as the expanded form's alpha2_j)
+template <int D>
+__global__ void row_scale_kernel(const float* __restrict__ X, int64_t n, float c2, float abar,
+                                 float* __restrict__ h) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float al = 0.f;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const float x = X[j * D + c];
+    al = fmaf(x, x, al);
   }
-  else if (r4 <= 512) { *nt = 512; *nv = 1; *tr = 8; }
-  else {
-    *nt = 512; *nv = 2; *tr = 4;
-    if (const char* e = getenv("LSK_ITR")) *tr = atoi(e) == 2 ? 2 : 4;   // tuning knob
-  }
+  h[j] = ex2(al * c2 - abar);
 }
 
-#define LSK_IMPL2(X, TS, TM, NV, TR) X(TS, TM, NV, TR, 1) X(TS, TM, NV, TR, 2) \
-  X(TS, TM, NV, TR, 3) X(TS, TM, NV, TR, 4) X(TS, TM, NV, TR, 5) X(TS, TM, NV, TR, 6)     \
-  X(TS, TM, NV, TR, 7) X(TS, TM, NV, TR, 8)
-#define LSK_IMPL2_ALL(X) LSK_IMPL2(X, 256, 2, 1, 8) LSK_IMPL2(X, 128, 4, 2, 4) LSK_IMPL2(X, 512, 1, 1, 8) \
-  LSK_IMPL2(X, 512, 1, 2, 2) LSK_IMPL2(X, 512, 1, 2, 4)
+template <int TS, int TEAMS, int NV, int TR, int D>
+constexpr size_t dyn_smem() {
+  return sizeof(double) * NV * 4 * TS * TEAMS + sizeof(float) * TEAMS * kRing * Geo<D>::SLOT +
+         sizeof(float4) * NV * TS;
+}
+
+}  // namespace impl
+
+// (TS, TEAMS, NV, TR, PIPE) per r, one CTA per SM.  PIPE = 1 holds two feature tiles (lag-one
+// software pipeline) and needs <= 256 threads for the registers; PIPE = 0 hides the exchange
+// latency with more warps instead (512 threads, one tile in registers).
+//   r <= 1024: four 128-thread teams, 8 columns per thread, 4-row tiles;
+//   r <= 2048: one 512-thread team, 4 columns per thread, 8-row tiles;
+//   r <= 4096: one 512-thread team, 8 columns per thread, 4-row tiles.
+// LSK_ICFG="ts,teams,nv,tr,pipe" selects another instantiated configuration (tuning knob).
+ImplCfg implicit_config(int r, int d) {
+  const int r4 = (r + 3) / 4;
+  ImplCfg c{};
+  {
+    // the warp-private kernel is opt-in (LSK_IWARP=1): measured slower than the team kernel on
+    // config 2 (26.6 vs 24.0 us per pass, DESIGN.md §6 K5)
+    const char* e = getenv("LSK_IWARP");
+    int nw, nv, tr;
+    if (e && atoi(e) == 1 && implicit_warp_config(r, d, &nw, &nv, &tr)) {
+      c.ts = 32 * nw; c.teams = 1; c.nv = nv; c.tr = tr; c.pipe = 0; c.warp = 1;
+      return c;
+    }
+  }
+  if (r4 <= 256) c = {128, 4, 2, 4, 0, 0};
+  else if (r4 <= 512) c = {512, 1, 1, 8, 0, 0};
+  else c = {512, 1, 2, 4, 0, 0};
+  if (const char* e = getenv("LSK_ICFG")) {
+    ImplCfg x{};
+    if (sscanf(e, "%d,%d,%d,%d,%d", &x.ts, &x.teams, &x.nv, &x.tr, &x.pipe) == 5 &&
+        x.ts * x.nv * 4 >= r)
+      c = x;
+  }
+  return c;
+}
+
+#define LSK_IMPL_D(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 1) X(TS, TM, NV, TR, P, 2) \
+  X(TS, TM, NV, TR, P, 3) X(TS, TM, NV, TR, P, 4) X(TS, TM, NV, TR, P, 5)                  \
+  X(TS, TM, NV, TR, P, 6) X(TS, TM, NV, TR, P, 7) X(TS, TM, NV, TR, P, 8)
+#define LSK_IMPL_D23(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 2) X(TS, TM, NV, TR, P, 3)
+// defaults for every d, then tuning alternatives for d = 2, 3
+#define LSK_IMPL_ALL(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
+  LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                     \
+  LSK_IMPL_D23(X, 128, 2, 2, 4, 1) LSK_IMPL_D23(X, 256, 1, 2, 4, 1) LSK_IMPL_D23(X, 256, 1, 4, 2, 1)
+
+template <int TS, int TM, int NV, int TR, int D, bool FACT, bool PIPE>
+static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, FACT, PIPE>;
+  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  if (coop) {
+    void* args[] = {(void*)&a};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS * TM), args, dyn, s);
+  } else {
+    kern<<<grid, TS * TM, dyn, s>>>(a);
+    e = cudaGetLastError();
+  }
+  count_launch();
+  return e;
+}
+
+template <int TS, int TM, int NV, int TR, int D, bool FACT, bool PIPE>
+static int occupancy_cfg() {
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, FACT, PIPE>;
+  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
+  int nb = 0;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TS * TM, dyn);
+  return nb;
+}
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
-  int ts, nv, tr;
-  implicit_config(a.r, &ts, &nv, &tr);
-#define X(TS_, TM_, NV_, TR_, D_)                                                              \
-  if (ts == TS_ && nv == NV_ && tr == TR_ && a.d == D_) {                                      \
-    auto kern = impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>;                                 \
-    const size_t dyn = sizeof(double) * NV_ * 4 * TS_ * TM_;                                   \
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn); \
-    if (e != cudaSuccess) return e;                                                            \
-    if (coop) {                                                                                \
-      void* args[] = {(void*)&a};                                                              \
-      e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS_ * TM_), args, dyn, s); \
-    } else {                                                                                   \
-      kern<<<grid, TS_ * TM_, dyn, s>>>(a);                                                    \
-      e = cudaGetLastError();                                                                  \
-    }                                                                                          \
-    count_launch();                                                                            \
-    return e;                                                                                  \
-  }
-  LSK_IMPL2_ALL(X)
+  const ImplCfg c = implicit_config(a.r, a.d);
+  if (c.warp) return launch_implicit_warp(a, coop, grid, s, nullptr);
+  const bool fact = a.hrow[0] != nullptr;
+#define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
+  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) \
+    return fact ? launch_cfg<TS_, TM_, NV_, TR_, D_, true, P_>(a, coop, grid, s)               \
+                : launch_cfg<TS_, TM_, NV_, TR_, D_, false, P_>(a, coop, grid, s);
+  LSK_IMPL_ALL(X)
 #undef X
   return cudaErrorInvalidConfiguration;
 }
 
-int implicit_max_ctas_per_sm(int r, int d) {
-  int ts, nv, tr;
-  implicit_config(r, &ts, &nv, &tr);
-#define X(TS_, TM_, NV_, TR_, D_)                                                              \
-  if (ts == TS_ && nv == NV_ && tr == TR_ && d == D_) {                                        \
-    int nb = 0;                                                                                \
-    const size_t dyn = sizeof(double) * NV_ * 4 * TS_ * TM_;                                   \
-    cudaFuncSetAttribute(impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>,                        \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);               \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, impl::implicit_kernel<TS_, TM_, NV_, TR_, D_>, TS_ * TM_, dyn); \
-    return nb;                                                                                 \
+int implicit_max_ctas_per_sm(const SinkArgs& a) {
+  const ImplCfg c = implicit_config(a.r, a.d);
+  if (c.warp) {
+    int occ = 0;
+    return launch_implicit_warp(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0;
   }
-  LSK_IMPL2_ALL(X)
+  const bool fact = a.hrow[0] != nullptr;
+#define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
+  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) \
+    return fact ? occupancy_cfg<TS_, TM_, NV_, TR_, D_, true, P_>()                            \
+                : occupancy_cfg<TS_, TM_, NV_, TR_, D_, false, P_>();
+  LSK_IMPL_ALL(X)
 #undef X
   return 0;
+}
+
+cudaError_t launch_row_scale(const float* X, int64_t n, int d, float c2, float abar, float* h,
+                             cudaStream_t s) {
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  switch (d) {
+#define C(D_) case D_: impl::row_scale_kernel<D_><<<blocks, 256, 0, s>>>(X, n, c2, abar, h); break;
+    C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
+#undef C
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace lsk

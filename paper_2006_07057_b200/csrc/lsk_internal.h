@@ -61,6 +61,10 @@ struct SinkArgs {
   const float* Wt;         // [d][r]  W_kc = (4 log2e / eps) U_kc, transposed
   const float* beta2;      // [r]     log2e (-(2/eps)|U_k|^2 + |U_k|^2/(eps q) + log_scale)
   float c2;                // -2 log2e / eps
+  // implicit factored exponent (FACT): F_jk = h_j * 2^(beta2_k + abar + sum_c W_kc p_jc),
+  // h_j = 2^(alpha2_j - abar) precomputed per row; NULL = plain expanded form
+  const float* hrow[2];
+  float abar;
   int dbg;                 // tuning only: 1 = consumers release stages without computing
   unsigned long long* trace;   // tuning only: [pass][cta][4] globaltimer stamps, or NULL
   float l2_resident;       // fraction of each CTA's rows per factor kept L2-resident (evict_last)
@@ -76,10 +80,20 @@ void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, in
 size_t sinkhorn_static_smem();
 int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t dyn_smem);
 
-// Implicit (recompute) kernel (lsk_implicit.cu): all-consumer CTAs, no dynamic smem.
-void implicit_config(int r, int* nt, int* nv, int* tr);
+// Implicit (recompute) kernel (lsk_implicit.cu): all-consumer CTAs, software-pipelined tiles.
+struct ImplCfg {
+  int ts, teams, nv, tr, pipe;
+  int warp;   // 1: warp-private kernel (lsk_implicit_warp.cu, r <= 1024)
+};
+ImplCfg implicit_config(int r, int d);
+bool implicit_warp_config(int r, int d, int* nwarp, int* nv, int* tr);
+cudaError_t launch_implicit_warp(const SinkArgs& a, bool cooperative, int grid, cudaStream_t s,
+                                 int* occ);
 cudaError_t launch_implicit(const SinkArgs& a, bool cooperative, int grid, cudaStream_t s);
-int implicit_max_ctas_per_sm(int r, int d);
+int implicit_max_ctas_per_sm(const SinkArgs& a);
+// h_j = 2^(c2 |p_j|^2 - abar) for the factored exponent (one launch per solve and side)
+cudaError_t launch_row_scale(const float* X, int64_t n, int d, float c2, float abar, float* h,
+                             cudaStream_t s);
 
 // Feature kernels (lsk_features.cu)
 cudaError_t launch_max_sqnorm(const float* X, int64_t n, int d, unsigned long long* out,

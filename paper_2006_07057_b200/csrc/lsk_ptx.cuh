@@ -138,6 +138,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// ---- MUFU rcp (rel. err ~2^-23; 0 -> inf, so a zero row dot still raises the breakdown) --
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void st_global_cs(float4* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)

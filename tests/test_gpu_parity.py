@@ -140,6 +140,34 @@ def test_config2_reduced_ragged(L, variant):
     _check_parity(res, ref)
 
 
+@pytest.mark.parametrize("fact", ["0", "1"])
+@pytest.mark.parametrize("cfg_key,n,m,T,env", [
+    (2, 4099, 3907, 200, {}),                                   # team kernel (128,4,2,4)
+    (2, 4099, 3907, 200, {"LSK_IWARP": "1"}),                   # warp-private kernel (8,8,1)
+    (2, 4099, 3907, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,8,2"}),
+    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,8,1"}),
+    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,4,1"}),
+    (2, 4099, 3907, 200, {"LSK_ICFG": "256,1,2,4,1"}),
+    (5, 6151, 6143, 40, {}),                                    # team kernel (512,1,2,4)
+    (5, 6151, 6143, 40, {"LSK_ICFG": "256,1,4,2,1"}),
+    (1, 500, 500, 200, {}),
+    (1, 500, 500, 200, {"LSK_IWARP": "1"}),                     # warp-private (16,1,4)
+    (1, 500, 500, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,4,4"}),
+    (1, 500, 500, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "16,4,2"})])
+def test_implicit_exponent_forms_and_configs(L, monkeypatch, fact, cfg_key, n, m, T, env):
+    """The implicit kernels' factored exponent (LSK_FACT=1, DESIGN.md §6 K5) and the plain
+    expanded form (LSK_FACT=0), for the default and every instantiated tuning configuration
+    of the warp-private and the team kernel, against the oracle (ragged n, m: tail tiles)."""
+    monkeypatch.setenv("LSK_FACT", fact)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = synth.get_config(cfg_key)
+    prob = synth.make_problem(cfg, n=n, m=m)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
+    res = _run_gpu(L, prob, T, variant="implicit")
+    _check_parity(res, ref)
+
+
 def test_config3_reduced_dirichlet(L):
     cfg = synth.get_config(3)
     prob = synth.make_problem(cfg, n=3001, m=2999)
