@@ -319,8 +319,11 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.nstage = c.nstage;
   A.stage_floats = c.stage_floats;
   const int64_t rs = A.r + kExtra;
-  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * rs * c.gpp * batch));
-  A.svec = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * rs * batch));
+  // part: [batch][r + kExtra + 2][gpp] (the last two columns carry the read-out partials);
+  // svec: [batch][2][r + kExtra], armed with the all-ones sentinel (lsk_sink_common.cuh)
+  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * (rs + 2) * c.gpp * batch));
+  A.svec = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * 2 * rs * batch));
+  LSK_CU(cudaMemsetAsync(A.svec, 0xFF, sizeof(double) * 2 * rs * batch, s));
   A.state = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * kStateDoubles * batch));
   A.bar = reinterpret_cast<unsigned int*>(ws + cv.take(sizeof(unsigned int) * batch));
   A.vbuf1 = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * A.rows[1] * batch));

@@ -117,8 +117,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
 
   float4 s[NV];
   const int64_t rstride = r + kExtra;
-  double* part = A.part + (int64_t)prob * rstride * A.gpp;
-  double* svec = A.svec + (int64_t)prob * rstride;
+  double* part = A.part + (int64_t)prob * (rstride + 2) * A.gpp;   // [r + kExtra + 2][gpp]
   const bool multi = A.multi_launch != 0;
   unsigned int nbar = 0;
 
@@ -131,8 +130,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
         const int qk = pass_kind(q, A);
         double e_err, e_brk;
         if (A.gpp > 1) {
-          e_err = __ldcg(svec + r);
-          e_brk = __ldcg(svec + r + 1);
+          e_err = sv_load(sv_of(A, prob, q) + r, multi);
+          e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
         } else {
           e_err = S.ext[0];
           e_brk = S.ext[1];
@@ -174,8 +173,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (g < R4) {
           if (A.gpp > 1) {
-            const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g));
-            const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g + 2));
+            const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g, multi);
+            const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g + 2, multi);
             v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
           } else {   // element (4 j + q) * 32 + l holds column 4 (l + 32 j) + q
             const int l = g & 31, j = g >> 5;
@@ -406,10 +405,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
 #pragma unroll 4
         for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
         acc = warp_sum_f64(acc);
-        if (lane == 0) svec[k] = acc;
+        if (lane == 0) sv_publish(A, prob, p, k, acc);
       }
       if (trc) trc[2] = globaltimer();
-      if (!multi) group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[3] = globaltimer();
     } else {
       if (tid == 0) {
@@ -454,16 +452,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
     }
     if (A.gpp > 1) {
       if (tid == 0) {
-        part[cta] = la;
-        part[A.gpp + cta] = lb;
+        part[(int64_t)rstride * A.gpp + cta] = la;        // columns r+kExtra, r+kExtra+1:
+        part[(int64_t)(rstride + 1) * A.gpp + cta] = lb;  // never read by R2 (no race with it)
       }
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (cta == 0 && tid == 0) {
         la = 0.0;
         lb = 0.0;
         for (int c = 0; c < A.gpp; ++c) {
-          la += __ldcg(part + c);
-          lb += __ldcg(part + A.gpp + c);
+          la += __ldcg(part + (int64_t)rstride * A.gpp + c);
+          lb += __ldcg(part + (int64_t)(rstride + 1) * A.gpp + c);
         }
       }
     }

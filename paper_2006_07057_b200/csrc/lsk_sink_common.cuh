@@ -61,6 +61,53 @@ __device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int ta
   named_bar(1, NTHR);
 }
 
+// ---- cross-CTA r-vector exchange without a second barrier ----------------------------------
+// The fp64 result of pass p (R2) goes to svec buffer p & 1 of the problem ([2][r + kExtra]).
+// Its readers (the next pass) poll each value until it differs from the sentinel (all-ones
+// bits: a NaN that no arithmetic produces), so no group barrier is needed between R2 and the
+// next pass.  The R2 owner of a column re-arms the other buffer (pass p-1's result, whose
+// readers all passed this pass's barrier 1) — visible to the readers of pass p+1's result
+// through barrier 1 of pass p+1.  Multi-launch mode (NCCL all-reduce between launches) keeps
+// one buffer and plain loads: the launch boundary orders everything.
+constexpr unsigned long long kSvSentinel = ~0ull;
+
+__device__ __forceinline__ double* sv_of(const SinkArgs& A, int prob, int pass) {
+  double* base = A.svec + (int64_t)prob * 2 * (A.r + kExtra);
+  return (A.multi_launch || !(pass & 1)) ? base : base + (A.r + kExtra);
+}
+
+__device__ __forceinline__ double sv_load(const double* p, bool multi) {
+  if (multi) return __ldcg(p);
+  unsigned long long b;
+  for (;;) {   // back off between polls: early CTAs must not flood the L2 lines being written
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+    if (b != kSvSentinel) break;
+    __nanosleep(100);
+  }
+  return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ double2 sv_load2(const double* p, bool multi) {
+  if (multi) return __ldcg(reinterpret_cast<const double2*>(p));
+  unsigned long long b0, b1;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(b0), "=l"(b1) : "l"(p) : "memory");
+    if (b0 != kSvSentinel && b1 != kSvSentinel) break;
+    __nanosleep(100);
+  }
+  return make_double2(__longlong_as_double((long long)b0), __longlong_as_double((long long)b1));
+}
+
+// R2 owner: publish column k of pass p and re-arm the same column of pass p-1's buffer
+__device__ __forceinline__ void sv_publish(const SinkArgs& A, int prob, int pass, int k, double v) {
+  double* cur = sv_of(A, prob, pass);
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(cur + k), "d"(v) : "memory");
+  if (!A.multi_launch) {
+    double* prv = sv_of(A, prob, pass + 1);   // the other buffer
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(prv + k), "l"(kSvSentinel) : "memory");
+  }
+}
+
 __device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
   return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];
 }

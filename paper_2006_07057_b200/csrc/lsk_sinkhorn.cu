@@ -200,8 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   // running solve state (identical in every CTA of the problem)
   double stErr = __ldcg(stg_state + ST_ERR);
   double stBrk = __ldcg(stg_state + ST_BRK);
-  double* part = A.part + (int64_t)prob * rstride * A.gpp;
-  double* svec = A.svec + (int64_t)prob * rstride;
+  double* part = A.part + (int64_t)prob * (rstride + 2) * A.gpp;   // [r + kExtra + 2][gpp]
   unsigned int nbar = 0;   // group barriers passed for this problem in this launch
   int final_t = -1, conv = 0;
   double ferr = -1.0;
@@ -214,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       const int qk = pass_kind(q, A);
       double e_err, e_brk;
       if (A.gpp > 1) {
-        e_err = __ldcg(svec + r);
-        e_brk = __ldcg(svec + r + 1);
+        e_err = sv_load(sv_of(A, prob, q) + r, multi);
+        e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
       } else {
         e_err = S.ext[0];
         e_brk = S.ext[1];
@@ -257,8 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
-            const double2 lo = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j]));
-            const double2 hi = __ldcg(reinterpret_cast<const double2*>(svec + 4 * g[j] + 2));
+            const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j], multi);
+            const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j] + 2, multi);
             s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
           } else {
             s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -513,10 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 #pragma unroll 4
         for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
         acc = warp_sum_f64(acc);
-        if (lane == 0) svec[k] = acc;
+        if (lane == 0) sv_publish(A, prob, p, k, acc);
       }
       if (trc) trc[2] = globaltimer();   // R2 done
-      if (!multi) group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[3] = globaltimer();   // barrier 2 passed
     } else {
       if (tid == 0) {
@@ -562,16 +560,16 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     }
     if (A.gpp > 1) {
       if (tid == 0) {
-        part[cta] = la;
-        part[A.gpp + cta] = lb;
+        part[(int64_t)rstride * A.gpp + cta] = la;        // columns r+kExtra, r+kExtra+1:
+        part[(int64_t)(rstride + 1) * A.gpp + cta] = lb;  // never read by R2 (no race with it)
       }
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (cta == 0 && tid == 0) {
         la = 0.0;
         lb = 0.0;
         for (int c = 0; c < A.gpp; ++c) {
-          la += __ldcg(part + c);
-          lb += __ldcg(part + A.gpp + c);
+          la += __ldcg(part + (int64_t)rstride * A.gpp + c);
+          lb += __ldcg(part + (int64_t)(rstride + 1) * A.gpp + c);
         }
       }
     }
