@@ -26,6 +26,11 @@ Pins (tests/test_oracle_*.py) — every function below is pinned to something ou
                         rank-1 closed form (P11), marginals (P12), convergence (P13),
                         primal == dual (P14), gauge invariance (P15), dual range (P17)
   dual_estimate         P9/P10/P11/P14
+  accelerated_sinkhorn  (NEXT f4, Alg. 2) == Alg. 1's converged W_hat on random factored
+                        instances (independent algorithm, unique dual optimum); 2x2 and
+                        rank-one closed forms; weak duality at every iterate; accepted
+                        L <= 4 (phi is 2-smooth); plan marginals -> (a, b), unit mass
+                        (tests/test_oracle_accel.py)
   exact gaussian ROT    paper RE behaviour on the Fig. 1 setup (P16, qualitative: the
                         paper prints no numbers — "parity unpinned" for the RE values
                         themselves; only the sign/monotonic trends are asserted)
@@ -390,3 +395,99 @@ def feature_matrix_arccos(X, U, sigma: float, s: int, kappa: float) -> np.ndarra
     r = U.shape[0]
     ph = arccos_phi(X[None, :, :], U[:, None, :], sigma, s, kappa)[..., 0] / math.sqrt(r)
     return np.vstack([ph, np.full((1, X.shape[0]), math.sqrt(kappa))])
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT f4. Accelerated Sinkhorn (Alg. 2; Eq. dual-smooth)
+# ---------------------------------------------------------------------------------------
+def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
+                         Kt_mv: Callable[[np.ndarray], np.ndarray],
+                         a, b, eps: float, L0: float = 1.0, T: Optional[int] = None,
+                         tol: Optional[float] = None, max_iter: int = 100000) -> dict:
+    """Alg. 2 step by step, with the readings of DESIGN.md C22-C27:
+      C22  phi(eta) := -F_theta(eta)/eps = log<e^{eta1}, K e^{eta2}> - <eta1,a> - <eta2,b>
+           is the objective minimised; Eq. (dual-smooth)'s "<K e^{eta2}>" is <e^{eta1}, K e^{eta2}>.
+      C23  "lambda^k = tau_k zeta^k + (1-tau_k) zeta^k" reads lambda^k = tau_k zeta^k + (1-tau_k) eta^k.
+      C24  the duplicated "L_{k+1} = L_k/2" is one halving before the line search; each
+           rejected trial doubles L_{k+1} ("Set L_{k+1} = 2 L_{k+1}").
+      C25  the unchanged block: "eta_2^{k+1} = lambda_2^{k+1}" reads eta_2^{k+1} = lambda_2^k
+           (and symmetrically eta_1^{k+1} = lambda_1^k).
+      C26  "zeta^{k+1} = zeta^k - a_{k+1} grad F_theta(lambda^k)" and the acceptance test use
+           grad phi (the gradient of the minimised objective, C22).
+      C27  x_hat is kept through its marginals x_hat 1 and x_hat^T 1 (z is n x m); argmax ties
+           pick block 1.  Stopping (tolerance mode): |x_hat 1 - a|_1 + |x_hat^T 1 - b|_1 < tol.
+      C28  a, b in the simplex (the theorem's "a, b in Delta_n"): the weights are
+           divided by their fp64 sums first — with sum a != sum b, F_theta grows without bound
+           along the gauge direction (eta1 + t, eta2 - t) and Alg. 2 drifts.
+    Returns eta1, eta2, F = F_theta(eta) (= -eps phi(eta)), the primal marginals p1, p2,
+    per-iteration traces (F, accepted L, block, trials) and the iteration count."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    a = a / a.sum()                                                     # C28
+    b = b / b.sum()
+    n, m = a.shape[0], b.shape[0]
+
+    def phi(e1, e2):
+        return math.log(np.exp(e1) @ K_mv(np.exp(e2))) - e1 @ a - e2 @ b
+
+    # Init: A_0 = alpha_0 = 0, eta^0 = zeta^0 = lambda^0 = 0 (PAPER.md:700)
+    ak, Lk = 0.0, float(L0)
+    eta1, eta2 = np.zeros(n), np.zeros(m)
+    zet1, zet2 = np.zeros(n), np.zeros(m)
+    p1, p2 = np.zeros(n), np.zeros(m)
+    F_tr, L_tr, blk_tr, trials_tr = [], [], [], []
+    converged = False
+    n_iter = T if tol is None else max_iter
+    it = 0
+    for _ in range(n_iter):
+        L1 = Lk / 2.0                                                   # C24
+        trials = 0
+        while True:
+            trials += 1
+            a1 = 1.0 / (2.0 * L1) + math.sqrt(1.0 / (4.0 * L1 * L1) + ak * ak * Lk / L1)
+            tau = 1.0 / (a1 * L1)
+            lam1 = tau * zet1 + (1.0 - tau) * eta1                      # C23
+            lam2 = tau * zet2 + (1.0 - tau) * eta2
+            Kv = K_mv(np.exp(lam2))                                     # K e^{lambda2}
+            Ktu = Kt_mv(np.exp(lam1))                                   # K^T e^{lambda1}
+            c = float(np.exp(lam1) @ Kv)                                # <e^{l1}, K e^{l2}>
+            g1 = np.exp(lam1) * Kv / c - a                              # grad_1 phi(lambda)
+            g2 = np.exp(lam2) * Ktu / c - b                             # grad_2 phi(lambda)
+            n1, n2 = float(g1 @ g1), float(g2 @ g2)
+            blk = 1 if n1 >= n2 else 2                                  # argmax block (C27)
+            if blk == 1:
+                new1 = lam1 + np.log(a) - np.log(np.exp(lam1) * Kv)
+                new2 = lam2                                             # C25
+            else:
+                new1 = lam1
+                new2 = lam2 + np.log(b) - np.log(np.exp(lam2) * Ktu)
+            if phi(new1, new2) <= phi(lam1, lam2) - (n1 + n2) / (2.0 * L1):
+                zet1 = zet1 - a1 * g1                                   # C26
+                zet2 = zet2 - a1 * g2
+                # x_hat^{k+1} = (a_{k+1} c^{-1} z + L_k a_k^2 x_hat^k) / (L_{k+1} a_{k+1}^2)
+                p1 = (a1 * (np.exp(lam1) * Kv) / c + Lk * ak * ak * p1) / (L1 * a1 * a1)
+                p2 = (a1 * (np.exp(lam2) * Ktu) / c + Lk * ak * ak * p2) / (L1 * a1 * a1)
+                eta1, eta2 = new1, new2
+                ak, Lk = a1, L1
+                break
+            L1 = 2.0 * L1
+        it += 1
+        F_tr.append(-eps * phi(eta1, eta2))
+        L_tr.append(Lk)
+        blk_tr.append(blk)
+        trials_tr.append(trials)
+        if tol is not None and float(np.abs(p1 - a).sum() + np.abs(p2 - b).sum()) < tol:
+            converged = True
+            break
+    return dict(eta1=eta1, eta2=eta2, F=-eps * phi(eta1, eta2), p1=p1, p2=p2, iters=it,
+                F_trace=np.array(F_tr), L_trace=np.array(L_tr), blocks=np.array(blk_tr),
+                trials=np.array(trials_tr), converged=converged)
+
+
+def accelerated_sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, eps: float,
+                                  L0: float = 1.0, T=None, tol=None, max_iter=100000) -> dict:
+    """Alg. 2 on K_theta = xi^T zeta: every K application costs r(n+m)."""
+    xi = np.asarray(xi, dtype=np.float64)
+    zeta = np.asarray(zeta, dtype=np.float64)
+    return accelerated_sinkhorn(lambda v: xi.T @ (zeta @ v), lambda u: zeta.T @ (xi @ u), a, b,
+                                eps, L0, T, tol, max_iter)
