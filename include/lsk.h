@@ -210,6 +210,46 @@ lsk_status lsk_rot_gradient(const lsk_feature_params* p, const float* U, const f
                             const float* Zeta, const float* u, const float* v, float* gX,
                             float* gY, float* gU, void* stream);
 
+/* ---- NEXT f4: accelerated Sinkhorn (Alg. 2) ------------------------- */
+/* Maximises the smooth dual (Eq. dual-smooth)
+ *   F_theta(eta) = eps [<eta1,a> + <eta2,b> - log <e^{eta1}, K_theta e^{eta2}>]
+ * by accelerated alternating minimisation of phi = -F/eps with the adaptive line search
+ * L <- L/2, then doubling until phi(eta^{k+1}) <= phi(lambda^k) - |grad phi(lambda^k)|^2/(2L)
+ * (readings C22-C28).  K_theta = Xi Zeta^T is streamed from HBM: each trial
+ * applies it three times (zeta^T e^{l2}, then xi . and xi^T e^{l1} in one pass, then zeta .).
+ * a, b are put on the simplex in fp64 first (C28).  Dual vectors live in fp64; e^{lambda}
+ * enters the passes shifted by its maximum (fp32 weights in (0, 1]).
+ *   o->max_iters  iterations (accepted steps); o->tol > 0: stop once the averaged plan's
+ *                 marginal error |x_hat 1 - a|_1 + |x_hat^T 1 - b|_1 < tol;
+ *   o->L0         initial smoothness estimate (> 0; 1 is a good default, phi is 2-smooth).
+ * eta1 (n), eta2 (m): device fp64 outputs, the final dual point.  F_trace_host, L_trace_host
+ * (host, max_iters doubles) and blk_trace_host (host, max_iters int32, the block 1/2 chosen):
+ * per-iteration traces, each nullable.  rep (host, nullable).  Synchronises (the line search
+ * reads four scalars per trial).  Returns LSK_NOT_CONVERGED if tol > 0 was not reached. */
+typedef struct lsk_accel_opts {
+  int32_t max_iters;
+  int32_t reserved;
+  double tol;
+  double L0;
+} lsk_accel_opts;
+
+typedef struct lsk_accel_report {
+  int32_t iters;        /* accepted iterations                                            */
+  int32_t trials;       /* line-search trials (>= iters)                                  */
+  int32_t converged;    /* tol > 0 and reached                                            */
+  int32_t reserved;
+  double F;             /* F_theta(eta) at the returned dual point                         */
+  double L;             /* last accepted L                                                 */
+  double plan_err;      /* |x_hat 1 - a|_1 + |x_hat^T 1 - b|_1 of the averaged plan        */
+} lsk_accel_report;
+
+lsk_status lsk_accelerated_sinkhorn(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                    int32_t r, const float* a, const float* b, double eps,
+                                    const lsk_accel_opts* o, double* eta1, double* eta2,
+                                    double* F_trace_host, double* L_trace_host,
+                                    int32_t* blk_trace_host, lsk_accel_report* rep,
+                                    void* stream);
+
 /* ---- whole path with HOST buffers (end-to-end entry point) ---------------------------- */
 /* X_host (n x d), Y_host (m x d), a_host, b_host (host memory, pinned or pageable).  Copies
  * inputs to the device, runs a1-a9 (variant 0 = auto, 1 = streaming, 2 = implicit), copies

@@ -416,6 +416,9 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
            grad phi (the gradient of the minimised objective, C22).
       C27  x_hat is kept through its marginals x_hat 1 and x_hat^T 1 (z is n x m); argmax ties
            pick block 1.  Stopping (tolerance mode): |x_hat 1 - a|_1 + |x_hat^T 1 - b|_1 < tol.
+      C29  the acceptance test carries an fp64 rounding allowance of 1e-13 max(1, |phi(lambda)|):
+           near the optimum the required decrease |grad|^2/(2L) falls below the rounding of
+           phi itself, and a strict test would double L without bound.
       C28  a, b in the simplex (the theorem's "a, b in Delta_n"): the weights are
            divided by their fp64 sums first — with sum a != sum b, F_theta grows without bound
            along the gauge direction (eta1 + t, eta2 - t) and Alg. 2 drifts.
@@ -435,7 +438,7 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
     eta1, eta2 = np.zeros(n), np.zeros(m)
     zet1, zet2 = np.zeros(n), np.zeros(m)
     p1, p2 = np.zeros(n), np.zeros(m)
-    F_tr, L_tr, blk_tr, trials_tr = [], [], [], []
+    F_tr, L_tr, blk_tr, trials_tr, g_tr = [], [], [], [], []
     converged = False
     n_iter = T if tol is None else max_iter
     it = 0
@@ -461,7 +464,8 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
             else:
                 new1 = lam1
                 new2 = lam2 + np.log(b) - np.log(np.exp(lam2) * Ktu)
-            if phi(new1, new2) <= phi(lam1, lam2) - (n1 + n2) / (2.0 * L1):
+            ph_lam = phi(lam1, lam2)
+            if phi(new1, new2) <= ph_lam - (n1 + n2) / (2.0 * L1) + 1e-13 * max(1.0, abs(ph_lam)):
                 zet1 = zet1 - a1 * g1                                   # C26
                 zet2 = zet2 - a1 * g2
                 # x_hat^{k+1} = (a_{k+1} c^{-1} z + L_k a_k^2 x_hat^k) / (L_{k+1} a_{k+1}^2)
@@ -476,12 +480,14 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
         L_tr.append(Lk)
         blk_tr.append(blk)
         trials_tr.append(trials)
+        g_tr.append((n1, n2))
         if tol is not None and float(np.abs(p1 - a).sum() + np.abs(p2 - b).sum()) < tol:
             converged = True
             break
     return dict(eta1=eta1, eta2=eta2, F=-eps * phi(eta1, eta2), p1=p1, p2=p2, iters=it,
                 F_trace=np.array(F_tr), L_trace=np.array(L_tr), blocks=np.array(blk_tr),
-                trials=np.array(trials_tr), converged=converged)
+                trials=np.array(trials_tr), grad_norms=np.array(g_tr).reshape(-1, 2),
+                converged=converged)
 
 
 def accelerated_sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, eps: float,

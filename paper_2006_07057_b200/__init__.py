@@ -53,6 +53,19 @@ class lsk_report(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
+class lsk_accel_opts(ctypes.Structure):
+    _fields_ = [("max_iters", c_i32), ("reserved", c_i32), ("tol", ctypes.c_double),
+                ("L0", ctypes.c_double)]
+
+
+class lsk_accel_report(ctypes.Structure):
+    _fields_ = [("iters", c_i32), ("trials", c_i32), ("converged", c_i32), ("reserved", c_i32),
+                ("F", ctypes.c_double), ("L", ctypes.c_double), ("plan_err", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
 P = ctypes.POINTER
 _SIGS = {
     "lsk_version": (ctypes.c_char_p, []),
@@ -98,6 +111,11 @@ _SIGS = {
     "lsk_rot_gradient": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p, c_i64,
                                  c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p,
                                  ctypes.c_void_p]),
+    "lsk_accelerated_sinkhorn": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
+                                         ctypes.c_double, P(lsk_accel_opts), ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, P(lsk_accel_report),
+                                         ctypes.c_void_p]),
     "lsk_rot_host": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
                              ctypes.c_double, c_i32, ctypes.c_uint64, ctypes.c_double,
                              P(lsk_solve_opts), c_i32, c_f32p, c_f32p, P(lsk_report)]),
@@ -316,6 +334,38 @@ def lsk_sinkhorn_divergence_implicit(p, U, X, Y, a, b, opts, stream=None):
                                                  _stream(stream)),
            "lsk_sinkhorn_divergence_implicit")
     return _div_result(out, reps)
+
+
+def lsk_accelerated_sinkhorn(Xi, Zeta, a, b, eps, max_iters, tol=0.0, L0=1.0, eta1=None,
+                             eta2=None, traces=False, stream=None):
+    """Alg. 2 on device factors Xi (n, r), Zeta (m, r).  Returns a dict with
+    the report fields, the fp64 dual point eta1 (n), eta2 (m) and, with traces=True, the
+    per-iteration F, accepted L and block."""
+    import torch
+    import numpy as np
+    n, m = Xi.shape[0], Zeta.shape[0]
+    if eta1 is None:
+        eta1 = torch.empty(n, dtype=torch.float64, device=Xi.device)
+    if eta2 is None:
+        eta2 = torch.empty(m, dtype=torch.float64, device=Xi.device)
+    o = lsk_accel_opts(int(max_iters), 0, float(tol), float(L0))
+    rep = lsk_accel_report()
+    tr = None
+    if traces:
+        tr = (np.zeros(max_iters), np.zeros(max_iters), np.zeros(max_iters, np.int32))
+    ptr = (lambda x: x.ctypes.data) if traces else (lambda x: None)
+    st = _lib.lsk_accelerated_sinkhorn(_f32(Xi), n, _f32(Zeta), m, Xi.shape[1], _f32(a),
+                                       _f32(b), float(eps), ctypes.byref(o), _ptr(eta1),
+                                       _ptr(eta2), ptr(tr[0]) if tr else None,
+                                       ptr(tr[1]) if tr else None, ptr(tr[2]) if tr else None,
+                                       ctypes.byref(rep), _stream(stream))
+    _check(st, "lsk_accelerated_sinkhorn")
+    out = rep.as_dict()
+    out.update(eta1=eta1, eta2=eta2, status=st)
+    if traces:
+        k = rep.iters
+        out.update(F_trace=tr[0][:k], L_trace=tr[1][:k], blocks=tr[2][:k])
+    return out
 
 
 def sinkhorn_divergence(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0,

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblsk.so")
-SOURCES = ["lsk_api.cu", "lsk_features.cu", "lsk_features_tc.cu", "lsk_sinkhorn.cu", "lsk_implicit.cu", "lsk_implicit_warp.cu", "lsk_grad.cu"]
+SOURCES = ["lsk_api.cu", "lsk_features.cu", "lsk_features_tc.cu", "lsk_sinkhorn.cu", "lsk_implicit.cu", "lsk_implicit_warp.cu", "lsk_grad.cu", "lsk_accel.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -732,6 +732,127 @@ static lsk_status divergence_impl(bool impl, const float* F, int64_t n, const fl
   return worst;
 }
 
+// ---------------------------------------------------------------- NEXT f4: Alg. 2 --------
+// Host side of the accelerated Sinkhorn line search (kernels and data flow: lsk_accel.cu).
+// Per trial: 1 lambda launch, 3 factor passes (+2 fixed-order r-vector reductions), 3
+// statistics launches, one synchronisation to read the per-CTA partials (summed here in a
+// fixed order — the device's block choice repeats the same sums), then the accept launch.
+lsk_status lsk_accelerated_sinkhorn(const float* Xi, int64_t n, const float* Zeta, int64_t m,
+                                    int32_t r, const float* a, const float* b, double eps,
+                                    const lsk_accel_opts* o, double* eta1, double* eta2,
+                                    double* F_trace, double* L_trace, int32_t* blk_trace,
+                                    lsk_accel_report* rep, void* stream) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (!Xi || !Zeta || !a || !b || !o || !eta1 || !eta2) return fail(LSK_EINVAL, "NULL argument");
+  if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
+  if (o->max_iters < 1 || !(o->L0 > 0.0)) return fail(LSK_EINVAL, "max_iters < 1 or L0 <= 0");
+  if (r > 2048) return fail(LSK_EDIM, "accelerated solver supports r <= 2048");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int G = accel_grid(), Gp = accel_pass_grid();
+  const int64_t mx = std::max(n, m);
+  Carve cv;
+  const size_t o_an = cv.take(8 * n), o_bn = cv.take(8 * m);
+  const size_t o_z1 = cv.take(8 * n), o_l1 = cv.take(8 * n), o_p1 = cv.take(8 * n), o_t1 = cv.take(8 * n);
+  const size_t o_z2 = cv.take(8 * m), o_l2 = cv.take(8 * m), o_p2 = cv.take(8 * m), o_t2 = cv.take(8 * m);
+  const size_t o_en = cv.take(8 * mx), o_pt = cv.take(8 * 6 * G), o_sc = cv.take(8 * 32),
+               o_tk = cv.take(256);
+  const size_t o_pa = cv.take(8 * (size_t)(Gp + 1) * r), o_pb = cv.take(8 * (size_t)(Gp + 1) * r);
+  char* ws;
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  auto D = [&](size_t off) { return reinterpret_cast<double*>(ws + off); };
+  AccelVecs v{};
+  v.n = n; v.m = m;
+  v.an = D(o_an); v.bn = D(o_bn);
+  v.eta1 = eta1; v.zet1 = D(o_z1); v.lam1 = D(o_l1); v.p1 = D(o_p1); v.t1 = D(o_t1);
+  v.eta2 = eta2; v.zet2 = D(o_z2); v.lam2 = D(o_l2); v.p2 = D(o_p2); v.t2 = D(o_t2);
+  v.etan = D(o_en); v.part = D(o_pt); v.scal = D(o_sc);
+  v.ticket = reinterpret_cast<unsigned int*>(ws + o_tk);
+  double* partA = D(o_pa);
+  double* partB = D(o_pb);
+  // Init: eta^0 = zeta^0 = 0, x_hat^0 = 0; simplex weights (C28)
+  LSK_CU(cudaMemsetAsync(eta1, 0, 8 * n, s));
+  LSK_CU(cudaMemsetAsync(eta2, 0, 8 * m, s));
+  LSK_CU(cudaMemsetAsync(v.zet1, 0, 8 * n, s));
+  LSK_CU(cudaMemsetAsync(v.zet2, 0, 8 * m, s));
+  LSK_CU(cudaMemsetAsync(v.p1, 0, 8 * n, s));
+  LSK_CU(cudaMemsetAsync(v.p2, 0, 8 * m, s));
+  LSK_CU(cudaMemsetAsync(v.ticket, 0, 256, s));
+  LSK_CU(launch_accel_normalise(a, b, v, s));
+
+  double sc[SC_COUNT];
+  double ak = 0.0, Lk = o->L0, F = 0.0, plan_err = -1.0;
+  int it = 0, trials = 0;
+  bool converged = false;
+  for (; it < o->max_iters;) {
+    double L1 = Lk / 2.0;   // C24: one halving, then doubling on rejection
+    double phi_new = 0.0;
+    int blk = 1;
+    for (;;) {
+      const double a1 = 1.0 / (2.0 * L1) + std::sqrt(1.0 / (4.0 * L1 * L1) + ak * ak * Lk / L1);
+      const double tau = 1.0 / (a1 * L1);
+      ++trials;
+      LSK_CU(launch_accel_lambda(tau, v, s));
+      // s2 = Zeta^T e^{l2 - M2};  t1 = Xi s2 and s1 = Xi^T e^{l1 - M1};  t2 = Zeta s1
+      LSK_CU(launch_accel_pass(Zeta, m, r, nullptr, v.lam2, v.scal + SC_M2, nullptr, partA, s));
+      LSK_CU(launch_accel_pass(Xi, n, r, partA + (size_t)Gp * r, v.lam1, v.scal + SC_M1, v.t1, partB, s));
+      LSK_CU(launch_accel_pass(Zeta, m, r, partB + (size_t)Gp * r, nullptr, nullptr, v.t2, nullptr, s));
+      LSK_CU(launch_accel_stats(1, v, 0, 0, 0, s));
+      LSK_CU(launch_accel_stats(2, v, 0, 0, 0, s));
+      LSK_CU(launch_accel_stats(3, v, 0, 0, 0, s));
+      LSK_CU(cudaMemcpyAsync(sc, v.scal, sizeof(sc), cudaMemcpyDeviceToHost, s));
+      LSK_CU(cudaStreamSynchronize(s));
+      const double M1 = sc[SC_M1], M2 = sc[SC_M2], S1 = sc[SC_S1], S2 = sc[SC_S2];
+      const double la = sc[SC_LA], lb = sc[SC_LB], n1 = sc[SC_N1], n2 = sc[SC_N2];
+      if (sc[SC_BAD] > 0.0 || !(S1 > 0.0) || !std::isfinite(S1) || !(S2 > 0.0))
+        return fail(LSK_EBREAKDOWN, "zero or non-finite K e^lambda during the accelerated solve");
+      blk = sc[SC_BLK] == 1.0 ? 1 : 2;                          // argmax, ties -> 1 (C27)
+      // phi(lambda^k), with c from the moved block's own side (the same t as phi(eta^{k+1}),
+      // so the exact block decrease stays >= 0 in floating point), and phi(eta^{k+1})
+      const double phi_lam = M1 + M2 + std::log(blk == 1 ? S1 : S2) - la - lb;
+      phi_new = std::log(sc[SC_E]) - (blk == 1 ? sc[SC_EW] + lb : la + sc[SC_EW]);
+      if (getenv("LSK_ADEBUG"))   // tuning/debug only
+        fprintf(stderr, "accel it %d L1 %.3g blk %d n %.3g %.3g phi %.12g -> %.12g\n", it, L1, blk,
+                n1, n2, phi_lam, phi_new);
+      // acceptance with an fp64 rounding allowance (reading C29)
+      if (phi_new <= phi_lam - (n1 + n2) / (2.0 * L1) + 1e-13 * std::max(1.0, std::fabs(phi_lam))) {
+        LSK_CU(launch_accel_stats(4, v, a1, Lk * ak * ak, L1 * a1 * a1, s));
+        ak = a1;
+        Lk = L1;
+        break;
+      }
+      L1 *= 2.0;
+      if (!(L1 < 1e300)) return fail(LSK_EBREAKDOWN, "line search diverged");
+    }
+    F = -eps * phi_new;
+    if (F_trace) F_trace[it] = F;
+    if (L_trace) L_trace[it] = Lk;
+    if (blk_trace) blk_trace[it] = blk;
+    ++it;
+    if (o->tol > 0.0 || it == o->max_iters) {
+      LSK_CU(cudaMemcpyAsync(&plan_err, v.scal + SC_PERR, 8, cudaMemcpyDeviceToHost, s));
+      LSK_CU(cudaStreamSynchronize(s));
+      if (o->tol > 0.0 && plan_err < o->tol) {
+        converged = true;
+        break;
+      }
+    }
+  }
+  if (rep) {
+    rep->iters = it;
+    rep->trials = trials;
+    rep->converged = converged ? 1 : 0;
+    rep->reserved = 0;
+    rep->F = F;
+    rep->L = Lk;
+    rep->plan_err = plan_err;
+  }
+  if (o->tol > 0.0 && !converged) {
+    g_err = "tolerance not reached within max_iters";
+    return LSK_NOT_CONVERGED;
+  }
+  return LSK_OK;
+}
+
 // ---------------------------------------------------------------- host-buffer pipeline --
 lsk_status lsk_rot_host(const float* X_host, int64_t n, const float* Y_host, int64_t m,
                         int32_t d, const float* a_host, const float* b_host, double eps,

@@ -128,6 +128,33 @@ cudaError_t launch_rot_value(const float* u, const float* v, const float* a, con
                              int64_t n, int64_t m, int batch, double* partials, double* out2,
                              cudaStream_t s);
 
+// accelerated Sinkhorn (lsk_accel.cu): fp64 device vectors of the line search
+enum AccelScalar {   // device scalar block, read by the host once per trial
+  SC_M1 = 0, SC_M2, SC_S1, SC_S2, SC_LA, SC_LB, SC_BAD, SC_N1, SC_N2, SC_BLK, SC_E, SC_EW,
+  SC_PERR, SC_COUNT
+};
+struct AccelVecs {
+  int64_t n, m;
+  double *an, *bn;                       // simplex weights
+  double *eta1, *zet1, *lam1, *p1, *t1;  // n
+  double *eta2, *zet2, *lam2, *p2, *t2;  // m
+  double *etan;                          // max(n, m): the moved block's minimiser
+  double *part;                          // per-CTA partials (>= 6 * accel_grid())
+  double *scal;                          // [SC_COUNT]
+  unsigned int* ticket;                  // last-CTA counter (zero between launches)
+};
+int accel_grid();
+int accel_pass_grid();
+cudaError_t launch_accel_normalise(const float* a, const float* b, const AccelVecs& v,
+                                   cudaStream_t s);
+cudaError_t launch_accel_lambda(double tau, const AccelVecs& v, cudaStream_t s);
+cudaError_t launch_accel_pass(const float* F, int64_t rows, int r, const double* s_in,
+                              const double* lam, const double* Mp, double* t_out, double* part,
+                              cudaStream_t s);
+// phase 1, 2, 3: statistics of the trial; phase 4: the accepted step
+cudaError_t launch_accel_stats(int phase, const AccelVecs& v, double a1, double Ak, double Ak1,
+                               cudaStream_t s);
+
 // Launch counter (host, thread-local) used for the bench's gpu_launches claim.
 void count_launch(int k = 1);
 

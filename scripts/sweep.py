@@ -47,6 +47,23 @@ p = L.lsk_feature_params_init(cfg.eps, d, r, 0.0, cfg.anchor_seed, X, Y)
 U = torch.empty((r, d), device="cuda"); L.lsk_draw_anchors(p, U)
 u = torch.empty(n, device="cuda"); v = torch.empty(m, device="cuda")
 opts = L.make_opts(a.T, 0.0, False, a.cps)
+if a.variant == "accel":   # Alg. 2: three factor passes per line-search trial
+    Xi = torch.empty((n, r), device="cuda"); Ze = torch.empty((m, r), device="cuda")
+    L.lsk_feature_map(p, U, X, Xi); L.lsk_feature_map(p, U, Y, Ze)
+    reps = []
+    def run():
+        reps.append(L.lsk_accelerated_sinkhorn(Xi, Ze, A_, B_, cfg.eps, a.T))
+    run(); torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); run(); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
+    ms = min(ts); tr = reps[-1]["trials"]
+    pass_bytes = 4.0 * r * (2 * m + n) * tr      # bytes the three passes of every trial read
+    print(json.dumps(dict(variant="accel", n=n, r=r, T=a.T, trials=tr, ms=round(ms, 3),
+                          us_per_iter=round(1e3 * ms / a.T, 2), us_per_trial=round(1e3 * ms / tr, 2),
+                          pass_GBs=round(pass_bytes / ms / 1e6), F=reps[-1]["F"])))
+    sys.exit(0)
 if a.variant == "stream":
     Xi = torch.empty((n, r), device="cuda"); Ze = torch.empty((m, r), device="cuda")
     L.lsk_feature_map(p, U, X, Xi); L.lsk_feature_map(p, U, Y, Ze)

@@ -443,3 +443,74 @@ def test_arccos_features_and_solve(L, d, s_deg, n):
     rot_ref = O.dual_estimate(sol["u"], sol["v"], a, b, eps)
     assert abs(rep.rot - rot_ref) <= ROT_TOL * abs(rot_ref)
     assert _maxrel(u, sol["u"]) <= UV_TOL and _maxrel(v, sol["v"]) <= UV_TOL
+
+
+# ------------------------------------------------------------------ NEXT f4: Alg. 2 -------
+def _accel_pair(L, cfg_key, n, m, T):
+    import torch
+    cfg = synth.get_config(cfg_key)
+    prob = synth.make_problem(cfg, n=n, m=m)
+    R = O.max_norm(prob["X"], prob["Y"])
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, cfg.r, R, cfg.anchor_seed)
+    U = torch.empty((cfg.r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((n, cfg.r), dtype=torch.float32, device="cuda")
+    Ze = torch.empty((m, cfg.r), dtype=torch.float32, device="cuda")
+    L.lsk_feature_map(p, U, _dev(prob["X"]), Xi)
+    L.lsk_feature_map(p, U, _dev(prob["Y"]), Ze)
+    gpu = L.lsk_accelerated_sinkhorn(Xi, Ze, _dev(prob["a"]), _dev(prob["b"]), cfg.eps, T,
+                                     traces=True)
+    Uo = O.draw_anchors(cfg.r, cfg.d, O.gaussian_params(cfg.eps, cfg.d, cfg.r, R)["sigma"],
+                        cfg.anchor_seed)
+    xi = O.feature_matrix(prob["X"], Uo, cfg.eps, p.q)
+    zeta = O.feature_matrix(prob["Y"], Uo, cfg.eps, p.q)
+    ref = O.accelerated_sinkhorn_factored(xi, zeta, prob["a"], prob["b"], cfg.eps, T=T)
+    return gpu, ref, (xi, zeta, prob, cfg)
+
+
+@pytest.mark.parametrize("cfg_key,n,m,T", [(1, 500, 500, 60), (2, 4099, 3907, 60),
+                                           (3, 3001, 2999, 40)])
+def test_accelerated_matches_oracle(L, cfg_key, n, m, T):
+    """Alg. 2 through the C ABI vs the oracle on the same seeded inputs.  The line search's
+    decisions (block i_k = argmax |grad_i phi|, accepted L) are floating-point decisions taken
+    on gradients g = e^lambda o K e^lambda' / c - a: fp32 factors perturb each entry by
+    ~1e-7 a_i, i.e. |g|^2 by ~2e-7 |a| |g| — they must agree exactly while the oracle's margin
+    |n1 - n2| / (n1 + n2) exceeds 100x that noise; beyond the first such near-tie the paths
+    may part, and only F (whose changes are O(|g|^2) there) is compared.  F per iteration
+    within 1e-5; the dual point (gauge-fixed: eta1 - eta1[0], eta2 + eta1[0]) within 1e-4
+    when no near-tie occurred."""
+    gpu, ref, (xi, zeta, prob, cfg) = _accel_pair(L, cfg_key, n, m, T)
+    assert gpu["iters"] == T
+    g = ref["grad_norms"]
+    a = prob["a"].astype(np.float64); a /= a.sum()
+    b = prob["b"].astype(np.float64); b /= b.sum()
+    noise = 2e-7 * np.maximum(np.linalg.norm(a) / np.sqrt(g[:, 0]), np.linalg.norm(b) / np.sqrt(g[:, 1]))
+    ties = np.nonzero(np.abs(g[:, 0] - g[:, 1]) <= 100 * noise * (g[:, 0] + g[:, 1]))[0]
+    k = int(ties[0]) if ties.size else T
+    assert k >= 5, "instance too close to a tie from the start"
+    assert np.array_equal(gpu["blocks"][:k], ref["blocks"][:k])
+    assert np.array_equal(gpu["L_trace"][:k], ref["L_trace"][:k])
+    assert np.max(np.abs(gpu["F_trace"] - ref["F_trace"]) / np.abs(ref["F_trace"])) <= 1e-5
+    if k == T:
+        e1 = gpu["eta1"].cpu().numpy()
+        e2 = gpu["eta2"].cpu().numpy()
+        g0, r0 = e1[0], ref["eta1"][0]
+        assert np.max(np.abs((e1 - g0) - (ref["eta1"] - r0))) <= 1e-4
+        assert np.max(np.abs((e2 + g0) - (ref["eta2"] + r0))) <= 1e-4
+
+
+def test_accelerated_converges_to_alg1(L):
+    """Tolerance mode on config 1: the accelerated solver's F reaches Alg. 1's converged
+    value (oracle, fp64) to 1e-5 relative, and stops on the plan-marginal tolerance."""
+    import torch
+    gpu, ref, (xi, zeta, prob, cfg) = _accel_pair(L, 1, 500, 500, 5)
+    a = prob["a"].astype(np.float64); a /= a.sum()
+    b = prob["b"].astype(np.float64); b /= b.sum()
+    s1 = O.sinkhorn_factored(xi, zeta, a, b, tol=1e-13, max_iter=100000)
+    W = O.dual_estimate(s1["u"], s1["v"], a, b, cfg.eps)
+    Xi = torch.from_numpy(xi.T.astype(np.float32).copy()).cuda()
+    Ze = torch.from_numpy(zeta.T.astype(np.float32).copy()).cuda()
+    res = L.lsk_accelerated_sinkhorn(Xi, Ze, _dev(prob["a"]), _dev(prob["b"]), cfg.eps, 20000,
+                                     tol=1e-4)
+    assert res["converged"] == 1 and res["plan_err"] < 1e-4
+    assert abs(res["F"] - W) <= 1e-5 * abs(W), (res["F"], W)
