@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) lam_kernel(double tau, AccelVecs v) 
 // <= 32 rows per warp, then fp64; warps combined in a fixed order).  One warp per row pair:
 // lane l holds float4 column groups {l, l+32, ...} (coalesced 512-byte loads per group).
 template <int NV, int ROWS>
-__global__ void __launch_bounds__(kThreads) pass_kernel(const float* __restrict__ F,
+__global__ void __launch_bounds__(kThreads, NV <= 8 ? 2 : 1) pass_kernel(const float* __restrict__ F,
                                                         int64_t rows, int r,
                                                         const double* __restrict__ s_in,
                                                         const double* __restrict__ lam,
@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const float* __restrict_
   const float4* s4 = reinterpret_cast<const float4*>(s_sm);
   for (int64_t row0 = r0 + (int64_t)warp * ROWS; row0 < r1; row0 += (int64_t)kWarps * ROWS) {
     float4 f[ROWS][NV];
+    double lr[ROWS];
     float w[ROWS];
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) lr[q] = (lam && row0 + q < r1) ? __ldg(lam + row0 + q) : -INFINITY;
 #pragma unroll
     for (int q = 0; q < ROWS; ++q) {
       const int64_t row = row0 + q;
@@ -159,8 +162,9 @@ __global__ void __launch_bounds__(kThreads) pass_kernel(const float* __restrict_
         const int g = lane + 32 * j;
         f[q][j] = (row < r1 && g < R4) ? __ldcs(Fr + g) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      w[q] = (lam && row < r1) ? (float)exp(lam[row] - M) : 0.f;
     }
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) w[q] = lam ? (float)exp(lr[q] - M) : 0.f;
 #pragma unroll
     for (int q = 0; q < ROWS; ++q) {
       const int64_t row = row0 + q;
