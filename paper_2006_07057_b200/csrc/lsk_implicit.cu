@@ -51,6 +51,14 @@ struct Geo {
   static constexpr int SLOT = 96 + 32 * XS;        // c[32] h[32] vold[32] x[32][XS]
 };
 
+// lanes per row in the row-dot exchange: the largest divisor of the team's warp count that
+// fits the lanes a row has after the transpose-reduce
+__host__ __device__ constexpr int exchange_lanes(int nwt, int lpr) {
+  int g = nwt < lpr ? nwt : lpr;
+  while (nwt % g) --g;
+  return g;
+}
+
 template <int TS, int TEAMS, int TR>
 struct Smem {
   uint64_t full[TEAMS][kRing];     // slot landed (32 cp.async arrivals of the loader warp)
@@ -72,7 +80,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   constexpr int XS = Geo<D>::XS, SLOT = Geo<D>::SLOT;
   constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;   // fp32 partial over <= 32 rows
   constexpr int LPR = 32 / TR;                                   // lanes per row after the transpose-reduce
-  constexpr int G = NWT < LPR ? NWT : LPR;                       // lanes per row in the exchange
+  constexpr int G = exchange_lanes(NWT, LPR);                     // lanes per row in the exchange
   constexpr int PER = NWT / G;                                   // partials summed per lane
   static_assert(TEAMS >= 1 && TEAMS <= 4, "1 to 4 teams");
   static_assert(TR * G <= 32 && NWT % G == 0, "exchange layout");
@@ -623,12 +631,14 @@ constexpr size_t dyn_smem() {
 
 }  // namespace impl
 
-// (TS, TEAMS, NV, TR, PIPE) per r, one CTA per SM.  PIPE = 1 holds two feature tiles (lag-one
-// software pipeline) and needs <= 256 threads for the registers; PIPE = 0 hides the exchange
-// latency with more warps instead (512 threads, one tile in registers).
-//   r <= 1024: four 128-thread teams, 8 columns per thread, 4-row tiles;
-//   r <= 2048: one 512-thread team, 4 columns per thread, 8-row tiles;
-//   r <= 4096: one 512-thread team, 8 columns per thread, 4-row tiles.
+// (TS, TEAMS, NV, TR, PIPE) per r and d, one CTA per SM.  Larger tiles amortise the per-tile
+// team exchange (measured, DESIGN.md §6 K5); they need the registers of fewer threads.
+// PIPE = 1 holds two feature tiles (lag-one software pipeline).
+//   r <= 1024, d <= 3: two 128-thread teams, 8 columns per thread, 16-row tiles (255 regs);
+//   r <= 1024, d > 3:  four 128-thread teams, 8 columns per thread, 4-row tiles;
+//   r <= 2048:         one 512-thread team, 4 columns per thread, 8-row tiles;
+//   r <= 4096, d <= 3: one 256-thread team, 16 columns per thread, 8-row tiles;
+//   r <= 4096, d > 3:  one 512-thread team, 8 columns per thread, 4-row tiles.
 // LSK_ICFG="ts,teams,nv,tr,pipe" selects another instantiated configuration (tuning knob).
 ImplCfg implicit_config(int r, int d) {
   const int r4 = (r + 3) / 4;
@@ -643,9 +653,9 @@ ImplCfg implicit_config(int r, int d) {
       return c;
     }
   }
-  if (r4 <= 256) c = {128, 4, 2, 4, 0, 0};
+  if (r4 <= 256) c = d <= 3 ? ImplCfg{128, 2, 2, 16, 0, 0} : ImplCfg{128, 4, 2, 4, 0, 0};
   else if (r4 <= 512) c = {512, 1, 1, 8, 0, 0};
-  else c = {512, 1, 2, 4, 0, 0};
+  else c = d <= 3 ? ImplCfg{256, 1, 4, 8, 0, 0} : ImplCfg{512, 1, 2, 4, 0, 0};
   if (const char* e = getenv("LSK_ICFG")) {
     ImplCfg x{};
     if (sscanf(e, "%d,%d,%d,%d,%d", &x.ts, &x.teams, &x.nv, &x.tr, &x.pipe) == 5 &&
@@ -658,11 +668,14 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_D(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 1) X(TS, TM, NV, TR, P, 2) \
   X(TS, TM, NV, TR, P, 3) X(TS, TM, NV, TR, P, 4) X(TS, TM, NV, TR, P, 5)                  \
   X(TS, TM, NV, TR, P, 6) X(TS, TM, NV, TR, P, 7) X(TS, TM, NV, TR, P, 8)
+#define LSK_IMPL_D123(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 1) X(TS, TM, NV, TR, P, 2) \
+  X(TS, TM, NV, TR, P, 3)
 #define LSK_IMPL_D23(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 2) X(TS, TM, NV, TR, P, 3)
-// defaults for every d, then tuning alternatives for d = 2, 3
+// defaults (every d; the big-tile ones for d <= 3), then tuning alternatives for d = 2, 3
 #define LSK_IMPL_ALL(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
-  LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                     \
-  LSK_IMPL_D23(X, 128, 2, 2, 4, 1) LSK_IMPL_D23(X, 256, 1, 2, 4, 1) LSK_IMPL_D23(X, 256, 1, 4, 2, 1)
+  LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                   \
+  LSK_IMPL_D123(X, 256, 1, 4, 8, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                  \
+  LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2)
 
 template <int TS, int TM, int NV, int TR, int D, bool FACT, bool PIPE>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {

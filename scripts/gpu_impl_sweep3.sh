@@ -1,0 +1,3 @@
+S="python scripts/sweep.py"
+for C in "128,3,2,8,0" "128,2,2,8,0" "128,2,2,16,0"; do echo "c2 $C"; LSK_ICFG=$C timeout 120 $S --config 2 --variant implicit --T 100; done
+for C in "256,2,2,4,0" "256,2,2,8,0" "384,1,3,8,0"; do echo "c5 $C"; LSK_ICFG=$C timeout 120 $S --config 5 --variant implicit --n 1048576 --T 2; done

@@ -142,13 +142,14 @@ def test_config2_reduced_ragged(L, variant):
 
 @pytest.mark.parametrize("fact", ["0", "1"])
 @pytest.mark.parametrize("cfg_key,n,m,T,env", [
-    (2, 4099, 3907, 200, {}),                                   # team kernel (128,4,2,4)
+    (2, 4099, 3907, 200, {}),                                   # team kernel (128,2,2,16)
+    (2, 4099, 3907, 200, {"LSK_ICFG": "128,4,2,4,0"}),
+    (2, 4099, 3907, 200, {"LSK_ICFG": "128,3,2,8,0"}),
     (2, 4099, 3907, 200, {"LSK_IWARP": "1"}),                   # warp-private kernel (8,8,1)
     (2, 4099, 3907, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,8,2"}),
-    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,8,1"}),
-    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,4,1"}),
-    (2, 4099, 3907, 200, {"LSK_ICFG": "256,1,2,4,1"}),
-    (5, 6151, 6143, 40, {}),                                    # team kernel (512,1,2,4)
+    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,8,1"}),         # lag-one pipeline
+    (5, 6151, 6143, 40, {}),                                    # team kernel (256,1,4,8)
+    (5, 6151, 6143, 40, {"LSK_ICFG": "512,1,2,4,0"}),
     (5, 6151, 6143, 40, {"LSK_ICFG": "256,1,4,2,1"}),
     (1, 500, 500, 200, {}),
     (1, 500, 500, 200, {"LSK_IWARP": "1"}),                     # warp-private (16,1,4)
