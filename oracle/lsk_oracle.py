@@ -200,7 +200,7 @@ def sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
              Kt_mv: Callable[[np.ndarray], np.ndarray],
              a: np.ndarray, b: np.ndarray, T: Optional[int] = None,
              tol: Optional[float] = None, max_iter: int = 100000,
-             record_err: bool = False) -> dict:
+             record_err: bool = False, u0: Optional[np.ndarray] = None) -> dict:
     """Alg. 1: inputs K, a, b, delta, u.  u^0 = 1_n (reading C6).  Repeat
     v <- b / K^T u ; u <- a / K v  until |v o K^T u - b|_1 < delta.
 
@@ -209,7 +209,7 @@ def sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
     Returns u, v, iters, errs (err_t per iteration when recorded), converged."""
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
-    u = np.ones(a.shape[0])
+    u = np.ones(a.shape[0]) if u0 is None else np.asarray(u0, dtype=np.float64)
     v = np.ones(b.shape[0])
     errs = []
     iters = 0
@@ -229,14 +229,14 @@ def sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
 
 
 def sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, T=None, tol=None,
-                      record_err=False, max_iter=100000) -> dict:
+                      record_err=False, max_iter=100000, u0=None) -> dict:
     """Alg. 1 with K_theta = xi^T zeta: K v = xi^T (zeta v),
     K^T u = zeta^T (xi u) — r(n+m) operations per application.
     xi is r x n, zeta is r x m (paper layout)."""
     xi = np.asarray(xi, dtype=np.float64)
     zeta = np.asarray(zeta, dtype=np.float64)
     return sinkhorn(lambda v: xi.T @ (zeta @ v), lambda u: zeta.T @ (xi @ u), a, b, T, tol,
-                    max_iter, record_err)
+                    max_iter, record_err, u0)
 
 
 def sinkhorn_dense(K: np.ndarray, a, b, T=None, tol=None, record_err=False,
@@ -497,3 +497,34 @@ def accelerated_sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, eps: f
     zeta = np.asarray(zeta, dtype=np.float64)
     return accelerated_sinkhorn(lambda v: xi.T @ (zeta @ v), lambda u: zeta.T @ (xi @ u), a, b,
                                 eps, L0, T, tol, max_iter)
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT f4 (second half). Small-eps stabilisation by row log-offsets (reading C30)
+# ---------------------------------------------------------------------------------------
+def feature_matrix_stabilized(X: np.ndarray, U: np.ndarray, eps: float, q: float):
+    """Row-normalised features: xi_tilde[:, i] = xi[:, i] / max_k xi[k, i] and the natural-log
+    offsets A_i = max_k log xi[k, i], so xi = xi_tilde e^{A} exactly (reading C30: Alg. 1 on
+    K_tilde = diag(e^-A) K diag(e^-B) from u_tilde^0 = 1 is Alg. 1 on K from u^0 = e^{-A},
+    "any arbitrary positive vector", PAPER.md:232 — same limit, and the same iterates as
+    from u^0 = 1 when started at u_tilde^0 = e^{A}).  Computed
+    from log phi (PAPER.md:934 written as an exponent), so nothing underflows before the
+    shift.  Returns (xi_tilde r x n, A n)."""
+    X = np.asarray(X, dtype=np.float64)
+    U = np.asarray(U, dtype=np.float64)
+    r, d = U.shape
+    logphi = ((d / 4.0) * math.log(2.0 * q)
+              - (2.0 / eps) * ((X[None, :, :] - U[:, None, :]) ** 2).sum(-1)
+              + (U ** 2).sum(-1)[:, None] / (eps * q)
+              - 0.5 * math.log(r))                                   # log(phi / sqrt(r)), r x n
+    A = logphi.max(axis=0)
+    return np.exp(logphi - A[None, :]), A
+
+
+def dual_estimate_offset(u_t, v_t, a, b, A, B, eps: float) -> float:
+    """W_hat from the scalings of the row-normalised problem: K = diag(e^A)
+    K_tilde diag(e^B) gives u = u_tilde e^{-A}, v = v_tilde e^{-B}, so
+    W_hat = eps (a^T (log u_tilde - A) + b^T (log v_tilde - B))."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return eps * (a @ (np.log(u_t) - A) + b @ (np.log(v_t) - B))
