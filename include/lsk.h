@@ -210,6 +210,22 @@ lsk_status lsk_rot_gradient(const lsk_feature_params* p, const float* U, const f
                             const float* Zeta, const float* u, const float* v, float* gX,
                             float* gY, float* gU, void* stream);
 
+/* ---- NEXT f4: small-eps stabilisation (reading C30) ------------------------ */
+/* Row-normalised Gaussian features: Xi (n x r) = xi / max_k xi_k (every row's largest entry
+ * is 1, so no row underflows fp32 at small eps) and logoff (n, fp64) = A_i = ln max_k xi_ik,
+ * i.e. xi = diag(e^A) Xi.  Alg. 1 on (Xi_x, Xi_y) returns u~ = u e^A, v~ = v e^B (it starts
+ * from u~ = 1, i.e. u = e^{-A}: "any positive vector"), and
+ *   W_hat = eps (a^T (log u~ - A) + b^T (log v~ - B))       (lsk_rot_value_offset).
+ * d <= 16 (LSK_EDIM otherwise).  Asynchronous. */
+lsk_status lsk_feature_map_stabilized(const lsk_feature_params* p, const float* U,
+                                      const float* X, int64_t n, float* Xi, double* logoff,
+                                      void* stream);
+/* W_hat of scalings u (n), v (m) of a row-normalised problem with offsets A (n), B (m) (device
+ * fp64).  rot_host: host double; synchronises. */
+lsk_status lsk_rot_value_offset(const float* u, const float* v, const float* a, const float* b,
+                                const double* A, const double* B, int64_t n, int64_t m,
+                                double eps, double* rot_host, void* stream);
+
 /* ---- NEXT f4: accelerated Sinkhorn (Alg. 2) ------------------------- */
 /* Maximises the smooth dual (Eq. dual-smooth)
  *   F_theta(eta) = eps [<eta1,a> + <eta2,b> - log <e^{eta1}, K_theta e^{eta2}>]

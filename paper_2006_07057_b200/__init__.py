@@ -111,6 +111,11 @@ _SIGS = {
     "lsk_rot_gradient": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p, c_i64,
                                  c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p,
                                  ctypes.c_void_p]),
+    "lsk_feature_map_stabilized": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_rot_value_offset": (c_i32, [c_f32p, c_f32p, c_f32p, c_f32p, ctypes.c_void_p,
+                                     ctypes.c_void_p, c_i64, c_i64, ctypes.c_double,
+                                     P(ctypes.c_double), ctypes.c_void_p]),
     "lsk_accelerated_sinkhorn": (c_i32, [c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p, c_f32p,
                                          ctypes.c_double, P(lsk_accel_opts), ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -336,6 +341,21 @@ def lsk_sinkhorn_divergence_implicit(p, U, X, Y, a, b, opts, stream=None):
     return _div_result(out, reps)
 
 
+def lsk_feature_map_stabilized(p, U, X, Xi, logoff, stream=None):
+    """Row-normalised features Xi (n, r) and fp64 row log-offsets logoff (n) (reading C30)."""
+    _check(_lib.lsk_feature_map_stabilized(ctypes.byref(p), _f32(U), _f32(X), X.shape[0],
+                                           _f32(Xi), _ptr(logoff), _stream(stream)),
+           "lsk_feature_map_stabilized")
+
+
+def lsk_rot_value_offset(u, v, a, b, A, B, eps, stream=None) -> float:
+    out = ctypes.c_double()
+    _check(_lib.lsk_rot_value_offset(_f32(u), _f32(v), _f32(a), _f32(b), _ptr(A), _ptr(B),
+                                     u.shape[0], v.shape[0], float(eps), ctypes.byref(out),
+                                     _stream(stream)), "lsk_rot_value_offset")
+    return out.value
+
+
 def lsk_accelerated_sinkhorn(Xi, Zeta, a, b, eps, max_iters, tol=0.0, L0=1.0, eta1=None,
                              eta2=None, traces=False, stream=None):
     """Alg. 2 on device factors Xi (n, r), Zeta (m, r).  Returns a dict with
@@ -440,9 +460,11 @@ def lsk_comm_destroy(comm):
 
 # ---------------------------------------------------------------- convenience -----------
 def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
-        want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None):
+        want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None, stabilize=False):
     """Whole hot path on device tensors: a1 params -> a2 anchors -> a3 features -> Alg. 1 ->
-    a9 read-out.  variant: "stream" (materialise xi, zeta) or "implicit" (recompute)."""
+    a9 read-out.  variant: "stream" (materialise xi, zeta) or "implicit" (recompute).
+    stabilize=True (stream, d <= 16): row-normalised features with log offsets (reading C30);
+    u, v are then the scalings of the normalised problem and A, B the offsets."""
     import torch
     dev = X.device
     d = X.shape[1]
@@ -461,9 +483,18 @@ def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
     else:
         Xi = torch.empty((n, r), dtype=torch.float32, device=dev)
         Zeta = torch.empty((m, r), dtype=torch.float32, device=dev)
-        lsk_feature_map(p, U, X, Xi, stream)
-        lsk_feature_map(p, U, Y, Zeta, stream)
+        if stabilize:
+            A = torch.empty(n, dtype=torch.float64, device=dev)
+            B = torch.empty(m, dtype=torch.float64, device=dev)
+            lsk_feature_map_stabilized(p, U, X, Xi, A, stream)
+            lsk_feature_map_stabilized(p, U, Y, Zeta, B, stream)
+            out.update(A=A, B=B)
+        else:
+            lsk_feature_map(p, U, X, Xi, stream)
+            lsk_feature_map(p, U, Y, Zeta, stream)
         rep = lsk_factored_sinkhorn(Xi, Zeta, a, b, eps, opts, u, v, comm=comm, stream=stream)
         out.update(Xi=Xi, Zeta=Zeta)
     out.update(report=rep.as_dict(), rot=rep.rot)
+    if variant != "implicit" and stabilize:
+        out["rot"] = lsk_rot_value_offset(u, v, a, b, out["A"], out["B"], eps, stream)
     return out

@@ -541,6 +541,43 @@ lsk_status lsk_feature_map(const lsk_feature_params* p, const float* U, const fl
   return feature_map_impl(p, U, X, n, Xi, static_cast<cudaStream_t>(stream));
 }
 
+lsk_status lsk_feature_map_stabilized(const lsk_feature_params* p, const float* U,
+                                      const float* X, int64_t n, float* Xi, double* logoff,
+                                      void* stream) {
+  if (!p || !U || !X || !Xi || !logoff) return fail(LSK_EINVAL, "NULL argument");
+  if (p->r < 4 || p->r % 4) return fail(LSK_EINVAL, "r must be a multiple of 4");
+  if (n < 1) return fail(LSK_EINVAL, "n must be >= 1");
+  if (p->d > 16) return fail(LSK_EDIM, "the stabilised feature map supports d <= 16");
+  if (!aligned16(Xi)) return fail(LSK_EINVAL, "Xi must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  Carve cv;
+  const size_t oD = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  float* bD = reinterpret_cast<float*>(ws + oD);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, nullptr, nullptr, bD, s));
+  LSK_CU(launch_feature_map_stab(X, n, p->d, U, bD, p->r, p->eps, Xi, logoff, s));
+  return LSK_OK;
+}
+
+lsk_status lsk_rot_value_offset(const float* u, const float* v, const float* a, const float* b,
+                                const double* A, const double* B, int64_t n, int64_t m,
+                                double eps, double* rot_host, void* stream) {
+  if (!u || !v || !a || !b || !A || !B || !rot_host) return fail(LSK_EINVAL, "NULL argument");
+  if (n < 1 || m < 1 || !(eps > 0)) return fail(LSK_EINVAL, "bad sizes or eps");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  LSK_TRY(get_ws(s, 8192 + 2 * 64 * sizeof(double), &ws));
+  double* part = reinterpret_cast<double*>(ws + 256);
+  double* out2 = reinterpret_cast<double*>(ws);
+  LSK_CU(launch_rot_value(u, v, a, b, n, m, 1, part, out2, s, A, B));
+  double h[2];
+  LSK_CU(cudaMemcpyAsync(h, out2, sizeof(h), cudaMemcpyDeviceToHost, s));
+  LSK_CU(cudaStreamSynchronize(s));
+  *rot_host = eps * (h[0] + h[1]);
+  return LSK_OK;
+}
+
 lsk_status lsk_feature_map_arccos(const lsk_feature_params* p, int32_t s_degree, double kappa,
                                   const float* U, const float* X, int64_t n, float* Xi,
                                   void* stream) {

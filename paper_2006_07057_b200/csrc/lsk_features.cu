@@ -243,6 +243,109 @@ cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- NEXT f4: stabilised ---
+// Row-normalised features (reading C30): with e2_ik = betaD_k + c2 |x_i - U_k|^2 (log2 of
+// phi/sqrt(r)), M_i = max_k e2_ik, write xi_tilde_ik = 2^(e2_ik - M_i) (every row's largest
+// entry is 1: no row can underflow) and the natural-log offset A_i = M_i ln 2 (fp64).
+// Block = 256 threads x 32 rows: pass 1 finds the 32 row maxima (registers, warp butterfly,
+// then 8 warp values in smem), pass 2 recomputes the exponents and writes.
+template <int D>
+__global__ void __launch_bounds__(256) feature_map_stab_kernel(
+    const float* __restrict__ X, int64_t n, const float* __restrict__ U,
+    const float* __restrict__ betaD, int r, float c2, float* __restrict__ Xi,
+    double* __restrict__ logoff) {
+  constexpr int RB = 32;
+  __shared__ float xs[RB][D];
+  __shared__ float wmax[8][RB];
+  __shared__ float rmax[RB];
+  const int64_t row0 = (int64_t)blockIdx.x * RB;
+  const int rows = (int)min((int64_t)RB, n - row0);
+  for (int i = threadIdx.x; i < rows * D; i += blockDim.x) xs[i / D][i % D] = X[row0 * D + i];
+  __syncthreads();
+  const int R4 = r >> 2;
+  float mx[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) mx[i] = -INFINITY;
+  for (int g = threadIdx.x; g < R4; g += blockDim.x) {
+    float u[4][D];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[q][c] = U[(int64_t)(4 * g + q) * D + c];
+    const float4 bd = *reinterpret_cast<const float4*>(betaD + 4 * g);
+    const float bq[4] = {bd.x, bd.y, bd.z, bd.w};
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float sq = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const float df = xs[i][c] - u[q][c];
+          sq = fmaf(df, df, sq);
+        }
+        mx[i] = fmaxf(mx[i], fmaf(c2, sq, bq[q]));
+      }
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    float v = mx[i];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wmax[warp][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < RB) {
+    float v = wmax[0][threadIdx.x];
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, wmax[w][threadIdx.x]);
+    rmax[threadIdx.x] = v;
+    if (threadIdx.x < rows) logoff[row0 + threadIdx.x] = (double)v * 0.69314718055994530942;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < R4; g += blockDim.x) {
+    float u[4][D];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < D; ++c) u[q][c] = U[(int64_t)(4 * g + q) * D + c];
+    const float4 bd = *reinterpret_cast<const float4*>(betaD + 4 * g);
+    const float bq[4] = {bd.x, bd.y, bd.z, bd.w};
+    for (int i = 0; i < rows; ++i) {
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float sq = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const float df = xs[i][c] - u[q][c];
+          sq = fmaf(df, df, sq);
+        }
+        o[q] = ex2(fmaf(c2, sq, bq[q]) - rmax[i]);
+      }
+      st_global_cs(reinterpret_cast<float4*>(Xi + (row0 + i) * r) + g, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+cudaError_t launch_feature_map_stab(const float* X, int64_t n, int d, const float* U,
+                                    const float* betaD, int r, double eps, float* Xi,
+                                    double* logoff, cudaStream_t s) {
+  const float c2 = (float)(-2.0 * kLog2e / eps);
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (int)((n + 31) / 32);
+  switch (d) {
+#define CASE(DD) case DD: feature_map_stab_kernel<DD><<<blocks, 256, 0, s>>>(X, n, U, betaD, r, c2, Xi, logoff); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- NEXT f3: arc-cosine ---
 // Xi[i][k] = coef_k relu(u_k . x_i)^s (k < r), Xi[i][r] = sqrt(kappa), Xi[i][r+1..r+3] = 0,
 // coef_k = sigma^{d/2} sqrt(2) exp(-|u_k|^2/4 (1 - 1/sigma^2)) / sqrt(r).
@@ -344,14 +447,18 @@ cudaError_t launch_const_cols(float* Xi, int64_t n, int ld, int col, float val, 
 constexpr int kRotBlocks = 64;
 __global__ void rot_partial_kernel(const float* __restrict__ u, const float* __restrict__ v,
                                    const float* __restrict__ a, const float* __restrict__ b,
-                                   int64_t n, int64_t m, double* partials) {
+                                   int64_t n, int64_t m, double* partials,
+                                   const double* __restrict__ offA,
+                                   const double* __restrict__ offB) {
   const int prob = blockIdx.z, side = blockIdx.y, blk = blockIdx.x;
   const int64_t len = side == 0 ? n : m;
   const float* w = side == 0 ? u + prob * n : v + prob * m;
   const float* c = side == 0 ? a + prob * n : b + prob * m;
+  const double* off = side == 0 ? offA : offB;   // stabilised read-out (C30): log u = log u~ - A
   const int64_t lo = len * blk / kRotBlocks, hi = len * (blk + 1) / kRotBlocks;
   double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += (double)c[i] * log((double)w[i]);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    acc += (double)c[i] * (log((double)w[i]) - (off ? off[prob * len + i] : 0.0));
   __shared__ double sh[256];
   sh[threadIdx.x] = acc;
   __syncthreads();
@@ -372,8 +479,9 @@ __global__ void rot_final_kernel(const double* partials, int batch, double* out2
 
 cudaError_t launch_rot_value(const float* u, const float* v, const float* a, const float* b,
                              int64_t n, int64_t m, int batch, double* partials, double* out2,
-                             cudaStream_t s) {
-  rot_partial_kernel<<<dim3(kRotBlocks, 2, batch), 256, 0, s>>>(u, v, a, b, n, m, partials);
+                             cudaStream_t s, const double* offA, const double* offB) {
+  rot_partial_kernel<<<dim3(kRotBlocks, 2, batch), 256, 0, s>>>(u, v, a, b, n, m, partials,
+                                                                 offA, offB);
   rot_final_kernel<<<(batch * 2 + 127) / 128, 128, 0, s>>>(partials, batch, out2);
   count_launch(2);
   return cudaGetLastError();

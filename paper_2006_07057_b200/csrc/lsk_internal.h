@@ -126,7 +126,12 @@ cudaError_t launch_gradients(const float* X, int64_t n, const float* Y, int64_t 
                              double* ws, cudaStream_t s);
 cudaError_t launch_rot_value(const float* u, const float* v, const float* a, const float* b,
                              int64_t n, int64_t m, int batch, double* partials, double* out2,
-                             cudaStream_t s);
+                             cudaStream_t s, const double* offA = nullptr,
+                             const double* offB = nullptr);
+// stabilised feature map (NEXT f4, reading C30), d <= 16
+cudaError_t launch_feature_map_stab(const float* X, int64_t n, int d, const float* U,
+                                    const float* betaD, int r, double eps, float* Xi,
+                                    double* logoff, cudaStream_t s);
 
 // accelerated Sinkhorn (lsk_accel.cu): fp64 device vectors of the line search
 enum AccelScalar {   // device scalar block, read by the host once per trial

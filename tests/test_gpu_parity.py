@@ -515,3 +515,55 @@ def test_accelerated_converges_to_alg1(L):
                                      tol=1e-4)
     assert res["converged"] == 1 and res["plan_err"] < 1e-4
     assert abs(res["F"] - W) <= 1e-5 * abs(W), (res["F"], W)
+
+
+# ------------------------------------------------------------------ NEXT f4: stabilisation -
+@pytest.mark.parametrize("eps", [0.1, 0.01])
+def test_stabilized_feature_map_matches_oracle(L, eps):
+    """Row-normalised features and their fp64 log offsets (reading C30) vs the oracle."""
+    import torch
+    cfg = synth.get_config(2)
+    n = 3001
+    prob = synth.make_problem(cfg, n=n, m=n)
+    R = O.max_norm(prob["X"], prob["Y"])
+    p = L.lsk_feature_params_init(eps, cfg.d, cfg.r, R, cfg.anchor_seed)
+    U = torch.empty((cfg.r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((n, cfg.r), dtype=torch.float32, device="cuda")
+    A = torch.empty(n, dtype=torch.float64, device="cuda")
+    L.lsk_feature_map_stabilized(p, U, _dev(prob["X"]), Xi, A)
+    torch.cuda.synchronize()
+    ref, Aref = O.feature_matrix_stabilized(prob["X"], U.cpu().double().numpy(), eps, p.q)
+    got = Xi.cpu().double().numpy()
+    assert np.all(got.max(axis=1) == 1.0)                      # every row's largest entry
+    mask = ref.T > 1e-30
+    rel = np.abs(got[mask] - ref.T[mask]) / ref.T[mask]
+    assert rel.max() <= 3e-5, rel.max()
+    assert np.max(np.abs(A.cpu().numpy() - Aref) / np.maximum(1.0, np.abs(Aref))) <= 1e-5
+
+
+@pytest.mark.parametrize("eps", [0.02, 0.01])
+def test_stabilized_small_eps_rot(L, eps):
+    """At eps where the plain fp32 path breaks down (0.01) or loses digits (0.02), the
+    stabilised stream path matches the fp64 oracle: W_hat within 1e-5 of the plain oracle's
+    value, and the scalings of the normalised problem within 1e-4 of the oracle run of the same
+    formulation (C30: Alg. 1 on the row-normalised factors from u~ = 1)."""
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=4000, m=3999)
+    T = 300
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], eps, cfg.r, cfg.anchor_seed, T=T)
+    res = _run_gpu_stab(L, prob, eps, T)
+    assert abs(res["rot"] - ref["rot"]) <= 1e-5 * abs(ref["rot"]), (res["rot"], ref["rot"])
+    R = O.max_norm(prob["X"], prob["Y"])
+    prm = O.gaussian_params(eps, cfg.d, cfg.r, R)
+    Uo = O.draw_anchors(cfg.r, cfg.d, prm["sigma"], cfg.anchor_seed)
+    xt, A = O.feature_matrix_stabilized(prob["X"], Uo, eps, prm["q"])
+    zt, B = O.feature_matrix_stabilized(prob["Y"], Uo, eps, prm["q"])
+    s = O.sinkhorn_factored(xt, zt, prob["a"], prob["b"], T=T)
+    assert _maxrel(res["u"], s["u"]) <= 1e-4 and _maxrel(res["v"], s["v"]) <= 1e-4
+
+
+def _run_gpu_stab(L, prob, eps, T):
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    cfg = synth.get_config(2)
+    return L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, stabilize=True)
