@@ -235,19 +235,19 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   c->impl = impl;
   c->batch = batch;
   const int hdr = 64 + 32 * 16;
-  int cps = (o && o->ctas_per_sm > 0) ? o->ctas_per_sm : (impl ? 2 : 1);
+  int cps = (o && o->ctas_per_sm > 0) ? o->ctas_per_sm : 1;
   const size_t static_smem = sinkhorn_static_smem();
   const size_t smem_sm = 227 * 1024;   // B200: 228 KB per SM, 227 KB usable per CTA
   int tr = 0, nv = 0, nst = 0, sf = 0;
   for (;; cps = 1) {
     const size_t per_cta =
         std::min<size_t>(max_smem_optin(), smem_sm / cps - (cps > 1 ? 1024 : 0)) - static_smem - 512;
-    sinkhorn_tile_config(A.r, impl, (int)(per_cta / 3), &tr, &nv);
-    sf = (hdr + (impl ? 0 : tr * A.r) + 31) & ~31;
-    nst = std::min<int>((int)(per_cta / ((size_t)sf * 4)), impl ? 8 : 16);
+    sinkhorn_tile_config(A.r, (int)(per_cta / 3), &tr, &nv);
+    sf = (hdr + tr * A.r + 31) & ~31;
+    nst = std::min<int>((int)(per_cta / ((size_t)sf * 4)), 16);
     if (nst >= 3 || cps == 1) break;
   }
-  if (nv > (impl ? 4 : 8)) return fail(LSK_EDIM, "r too large for this variant");
+  if (nv > 8) return fail(LSK_EDIM, "r too large for this variant");
   // the pipelined tile loop holds two stages while the producer fills a third
   if (nst < 3) return fail(LSK_EDIM, "r too large: three ring stages do not fit in shared memory");
   if (const char* e = getenv("LSK_NSTAGE")) nst = std::max(3, std::min(nst, atoi(e)));   // tuning knob
@@ -256,7 +256,7 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   c->stage_floats = sf;
   c->nstage = nst;
   c->smem = (size_t)nst * sf * 4;
-  int occ = sinkhorn_max_ctas_per_sm(impl, nv, tr, A.d, c->smem);
+  int occ = sinkhorn_max_ctas_per_sm(nv, tr, c->smem);
   if (occ < 1) return fail(LSK_EUNSUPPORTED, "sinkhorn kernel does not fit on an SM");
   cps = std::min(cps, occ);
   const int sms = num_sms();
@@ -340,7 +340,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     A.pass_end = A.num_passes;
     A.multi_launch = 0;
     LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
-    LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+    LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, c.coop, c.grid, c.smem, s));
   } else {
     if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
     A.multi_launch = 1;
@@ -349,7 +349,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       A.pass_end = std::min(p + 1, A.num_passes);
       if (p == A.num_passes) A.pass_end = p;   // finalise-only launch
       LSK_CU(cudaMemsetAsync(A.bar, 0, sizeof(unsigned int) * batch, s));
-      LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, impl, c.coop, c.grid, c.smem, s));
+      LSK_CU(impl ? launch_implicit(A, c.coop, c.grid, s) : launch_sinkhorn(A, c.coop, c.grid, c.smem, s));
       if (p < A.num_passes)
         LSK_TRY(nccl_check(nccl().allReduce(A.svec, A.svec, (size_t)rs * batch, ncclFloat64,
                                             ncclSum, comm->comm, s),

@@ -73,12 +73,12 @@ struct SinkArgs {
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.
-cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool cooperative, int grid,
-                            size_t smem, cudaStream_t s);
+cudaError_t launch_sinkhorn(const SinkArgs& a, bool cooperative, int grid, size_t smem,
+                            cudaStream_t s);
 // Kernel configuration for a given r / mode: rows per tile and stage floats.
-void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, int* nv);
+void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv);
 size_t sinkhorn_static_smem();
-int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t dyn_smem);
+int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t dyn_smem);
 
 // Implicit (recompute) kernel (lsk_implicit.cu): all-consumer CTAs, software-pipelined tiles.
 struct ImplCfg {

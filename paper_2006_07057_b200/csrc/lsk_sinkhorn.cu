@@ -21,9 +21,7 @@
 // <= 32 rows, then fp64; cross-CTA reduction in fp64 in a fixed order (deterministic, no
 // float atomics).  Marginal error and a^T log u / b^T log v in fp64.
 //
-// Implicit variant (template IMPL): no factor in HBM — the producer stages point rows x_j
-// and the consumers regenerate F_jk = 2^(alpha2_j + beta2_k + sum_c W_kc x_jc) with MUFU
-// ex2 in registers (expanded form of PAPER.md:934 in base 2).
+// The recompute (implicit) variant has its own kernels: lsk_implicit.cu.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -37,7 +35,8 @@ namespace lsk {
 
 constexpr int NT = kConsumerThreads;
 constexpr int NW = NT / 32;
-constexpr int kHdr = 64 + 32 * 16;   // stage header floats: c[32], vold[32], x[32][16]
+constexpr int kHdr = 64 + 32 * 16;   // stage header floats: c[32], vold[32], (pad) — keeps the
+                                     // factor rows 16-byte aligned after the header
 constexpr int kMaxStages = 16;
 
 struct Smem {
@@ -51,7 +50,7 @@ struct Smem {
   int stop_seq;   // base(k) once the k-th problem of the CTA has stopped (tolerance mode)
 };
 
-template <bool IMPL, int NV, int TR, int D>
+template <int NV, int TR>
 __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A) {
   extern __shared__ __align__(128) float ring[];
   __shared__ Smem S;
@@ -115,8 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
       const float* vold = nullptr;
       if (need_vold) vold = vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1);
-      const float* Fp = IMPL ? nullptr : A.F[f] + (int64_t)prob * A.fstride[f];
-      const float* Xp = IMPL ? A.X[f] + (int64_t)prob * A.fstride[f] : nullptr;
+      const float* Fp = A.F[f] + (int64_t)prob * A.fstride[f];
       // the first l2_resident of this CTA's rows stay in L2 across iterations (evict_last)
       const int64_t keep_end = r0 + (int64_t)((double)(r1 - r0) * (double)A.l2_resident);
       for (int64_t row0 = r0; row0 < r1; row0 += TR) {
@@ -124,21 +122,13 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         mbar_wait(&S.empty[stage], phase ^ 1u);
         float* st = ring + (int64_t)stage * A.stage_floats;
         if (lane == 0) {
-          if constexpr (!IMPL) {
-            const uint32_t bytes = (uint32_t)rows * (uint32_t)r * 4u;
-            mbar_arrive_expect_tx(&S.full[stage], bytes);
-            bulk_g2s(st + kHdr, Fp + row0 * r, bytes, &S.full[stage], row0 < keep_end ? pol_keep : pol);
-          } else {
-            mbar_arrive(&S.full[stage]);
-          }
+          const uint32_t bytes = (uint32_t)rows * (uint32_t)r * 4u;
+          mbar_arrive_expect_tx(&S.full[stage], bytes);
+          bulk_g2s(st + kHdr, Fp + row0 * r, bytes, &S.full[stage], row0 < keep_end ? pol_keep : pol);
         }
         if (lane < rows) {
           cp_async4(st + lane, wp + row0 + lane);
           if (need_vold) cp_async4(st + 32 + lane, vold + row0 + lane);
-          if constexpr (IMPL) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) cp_async4(st + 64 + lane * 16 + c, Xp + (row0 + lane) * D + c);
-          }
         }
         cp_async_mbar_arrive_noinc(&S.full[stage]);
         if (++stage == (uint32_t)A.nstage) {
@@ -163,23 +153,6 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     gv[j] = g[j] < R4;
     ge[j] = gv[j] ? g[j] : 0;
   }
-  float4 Wr[IMPL ? NV : 1][IMPL ? D : 1];
-  float4 b2[IMPL ? NV : 1];
-  if constexpr (IMPL) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      if (gv[j]) {
-        b2[j] = *reinterpret_cast<const float4*>(A.beta2 + 4 * g[j]);
-#pragma unroll
-        for (int c = 0; c < D; ++c) Wr[j][c] = *reinterpret_cast<const float4*>(A.Wt + (int64_t)c * r + 4 * g[j]);
-      } else {
-        b2[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-#pragma unroll
-        for (int c = 0; c < D; ++c) Wr[j][c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-  }
-
   float4 s[NV];
   double acc64[NV][4];
 #pragma unroll
@@ -291,19 +264,15 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     // Software-pipelined tile loop: tile k's row dots are reduced across warps through
     // red[k % 3] + an mbarrier (split arrive / wait), and finished (scaling, accumulation,
     // stage release) only after tile k+1's dots are issued — no CTA-wide barrier per tile.
-    float frA[IMPL ? TR : 1][IMPL ? NV : 1][4];
-    float frB[IMPL ? TR : 1][IMPL ? NV : 1][4];
     int64_t row0 = r0;
     bool pend = false;              // a tile whose dots are issued but not finished
-    bool pend_in_A = false;
     int64_t p_row0 = 0;
     int p_rows = 0;
     uint32_t p_stage = 0, p_tk = 0;
 
     // finish a tile: wait for all warps' partial dots, derive the TR scalings (every warp
     // computes them identically), write them (warp 0), accumulate F_j^T w_j, release the stage
-    auto finish = [&](float (&fr)[IMPL ? TR : 1][IMPL ? NV : 1][4], uint32_t fstage,
-                      int64_t frow0, int frows, uint32_t ftk) {
+    auto finish = [&](uint32_t fstage, int64_t frow0, int frows, uint32_t ftk) {
       const float* st = ring + (int64_t)fstage * A.stage_floats;
       const float* feat = st + kHdr;
       float vr_l = 0.f;
@@ -334,27 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         for (int i = 0; i < TR; ++i) vis[i] = __shfl_sync(0xffffffffu, vr_l, i);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          float4 fvv[IMPL ? 1 : TR];
-          if constexpr (!IMPL) {
+          float4 fvv[TR];
 #pragma unroll
-            for (int i = 0; i < TR; ++i)
-              fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
-          }
+          for (int i = 0; i < TR; ++i)
+            fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
             const float vi = vis[i];
-            if constexpr (IMPL) {
-              acc32[j].x = fmaf(fr[i][j][0], vi, acc32[j].x);
-              acc32[j].y = fmaf(fr[i][j][1], vi, acc32[j].y);
-              acc32[j].z = fmaf(fr[i][j][2], vi, acc32[j].z);
-              acc32[j].w = fmaf(fr[i][j][3], vi, acc32[j].w);
-            } else {
-              const float4 fv = fvv[i];
-              acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
-              acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
-              acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
-              acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
-            }
+            const float4 fv = fvv[i];
+            acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
+            acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
+            acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
+            acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
           }
         }
         if (++tiles_since_flush == kFlushTiles) {
@@ -373,9 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (lane == 0) mbar_arrive(&S.empty[fstage]);
     };
 
-    // issue tile at row0 into `cur`; then finish the pending tile (held in `prv`)
-    auto step = [&](float (&cur)[IMPL ? TR : 1][IMPL ? NV : 1][4],
-                    float (&prv)[IMPL ? TR : 1][IMPL ? NV : 1][4], bool cur_is_A) -> bool {
+    // issue the dots of the tile at row0; then finish the pending tile
+    auto step = [&]() -> bool {
       if (row0 >= r1) return false;
       const int rows = (int)min((int64_t)TR, r1 - row0);
       mbar_wait(&S.full[stage], phase);
@@ -388,33 +347,6 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       }
       const float* st = ring + (int64_t)stage * A.stage_floats;
       const float* feat = st + kHdr;
-      if constexpr (IMPL) {
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          float x[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) x[c] = st[64 + i * 16 + c];
-          float al = 0.f;
-#pragma unroll
-          for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
-          al *= A.c2;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-            float e0 = al + b2[j].x, e1 = al + b2[j].y, e2 = al + b2[j].z, e3 = al + b2[j].w;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              e0 = fmaf(Wr[j][c].x, x[c], e0);
-              e1 = fmaf(Wr[j][c].y, x[c], e1);
-              e2 = fmaf(Wr[j][c].z, x[c], e2);
-              e3 = fmaf(Wr[j][c].w, x[c], e3);
-            }
-            cur[i][j][0] = ex2(e0);
-            cur[i][j][1] = ex2(e1);
-            cur[i][j][2] = ex2(e2);
-            cur[i][j][3] = ex2(e3);
-          }
-        }
-      }
       uint32_t my_tk = tk;
       if (kind != PK_INIT) {
         // rows >= `rows` of a tail tile hold finite stale/zero data; their dots are unused
@@ -423,26 +355,17 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         for (int i = 0; i < TR; ++i) pr[i] = 0.f;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
-          float4 fvv[IMPL ? 1 : TR];
-          if constexpr (!IMPL) {
+          float4 fvv[TR];
 #pragma unroll
-            for (int i = 0; i < TR; ++i)   // all loads of this column group first
-              fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
-          }
+          for (int i = 0; i < TR; ++i)   // all loads of this column group first
+            fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
-            if constexpr (IMPL) {
-              pr[i] = fmaf(cur[i][j][0], s[j].x, pr[i]);
-              pr[i] = fmaf(cur[i][j][1], s[j].y, pr[i]);
-              pr[i] = fmaf(cur[i][j][2], s[j].z, pr[i]);
-              pr[i] = fmaf(cur[i][j][3], s[j].w, pr[i]);
-            } else {
-              const float4 fv = fvv[i];
-              pr[i] = fmaf(fv.x, s[j].x, pr[i]);
-              pr[i] = fmaf(fv.y, s[j].y, pr[i]);
-              pr[i] = fmaf(fv.z, s[j].z, pr[i]);
-              pr[i] = fmaf(fv.w, s[j].w, pr[i]);
-            }
+            const float4 fv = fvv[i];
+            pr[i] = fmaf(fv.x, s[j].x, pr[i]);
+            pr[i] = fmaf(fv.y, s[j].y, pr[i]);
+            pr[i] = fmaf(fv.z, s[j].z, pr[i]);
+            pr[i] = fmaf(fv.w, s[j].w, pr[i]);
           }
         }
         const float tot = warp_transpose_reduce<TR>(pr, lane);
@@ -452,9 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         mbar_arrive(&S.redbar[rb]);   // every consumer lane arrives (count NT)
         ++tk;
       }
-      if (pend) finish(prv, p_stage, p_row0, p_rows, p_tk);
+      if (pend) finish(p_stage, p_row0, p_rows, p_tk);
       pend = true;
-      pend_in_A = cur_is_A;
       p_stage = stage;
       p_row0 = row0;
       p_rows = rows;
@@ -466,12 +388,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       row0 += TR;
       return true;
     };
-    while (step(frA, frB, true) && step(frB, frA, false)) {
+    while (step()) {
     }
-    if (pend) {
-      if (pend_in_A) finish(frA, p_stage, p_row0, p_rows, p_tk);
-      else finish(frB, p_stage, p_row0, p_rows, p_tk);
-    }
+    if (pend) finish(p_stage, p_row0, p_rows, p_tk);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       acc64[j][0] += (double)acc32[j].x;
@@ -593,16 +512,12 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 }
 
 // ------------------------------------------------------------------------------------------
-void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, int* nv) {
+void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv) {
   const int r4 = (r + 3) / 4;
   int v = (r4 + NT - 1) / NT;
   int p2 = 1;
   while (p2 < v) p2 <<= 1;
   *nv = p2;
-  if (implicit) {
-    *tr = 4 / p2 > 0 ? 4 / p2 : 1;   // two tiles of regenerated features live in registers
-    return;
-  }
   // largest instantiated TR whose stage fits the budget (target 64 KB: long tiles amortise
   // the per-tile cross-warp exchange; measured on config 2: 32 KB stages 4.6 TB/s, 64 KB
   // stages 5.3 TB/s)
@@ -619,10 +534,10 @@ void sinkhorn_tile_config(int r, bool implicit, int max_stage_bytes, int* tr, in
 
 size_t sinkhorn_static_smem() { return sizeof(Smem); }
 
-template <bool IMPL, int NV, int TR, int D>
+template <int NV, int TR>
 static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
                             cudaStream_t s) {
-  auto kern = sinkhorn_kernel<IMPL, NV, TR, D>;
+  auto kern = sinkhorn_kernel<NV, TR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -637,10 +552,10 @@ static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
   return e;
 }
 
-template <bool IMPL, int NV, int TR, int D>
+template <int NV, int TR>
 static int occupancy_t(size_t smem) {
   int nb = 0;
-  auto kern = sinkhorn_kernel<IMPL, NV, TR, D>;
+  auto kern = sinkhorn_kernel<NV, TR>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
   return nb;
@@ -648,34 +563,19 @@ static int occupancy_t(size_t smem) {
 
 #define LSK_STREAM_CASES(X) X(1, 32) X(1, 16) X(1, 8) X(2, 16) X(2, 8) X(2, 4) X(4, 8) X(4, 4) \
   X(4, 2) X(8, 4) X(8, 2) X(8, 1)
-#define LSK_IMPL_D(X, NV, TR) X(NV, TR, 1) X(NV, TR, 2) X(NV, TR, 3) X(NV, TR, 4) \
-  X(NV, TR, 5) X(NV, TR, 6) X(NV, TR, 7) X(NV, TR, 8)
 
-cudaError_t launch_sinkhorn(const SinkArgs& a, bool implicit, bool coop, int grid, size_t smem,
-                            cudaStream_t s) {
+cudaError_t launch_sinkhorn(const SinkArgs& a, bool coop, int grid, size_t smem, cudaStream_t s) {
   const int tr = a.tr, nv = a.nv;
-  if (!implicit) {
-#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return launch_t<false, NV_, TR_, 1>(a, coop, grid, smem, s);
-    LSK_STREAM_CASES(X)
+#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return launch_t<NV_, TR_>(a, coop, grid, smem, s);
+  LSK_STREAM_CASES(X)
 #undef X
-  } else {
-#define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && a.d == D_) return launch_t<true, NV_, TR_, D_>(a, coop, grid, smem, s);
-    LSK_IMPL_D(X, 1, 4) LSK_IMPL_D(X, 2, 2) LSK_IMPL_D(X, 4, 1)
-#undef X
-  }
   return cudaErrorInvalidConfiguration;
 }
 
-int sinkhorn_max_ctas_per_sm(bool implicit, int nv, int tr, int d, size_t smem) {
-  if (!implicit) {
-#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return occupancy_t<false, NV_, TR_, 1>(smem);
-    LSK_STREAM_CASES(X)
+int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t smem) {
+#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return occupancy_t<NV_, TR_>(smem);
+  LSK_STREAM_CASES(X)
 #undef X
-  } else {
-#define X(NV_, TR_, D_) if (nv == NV_ && tr == TR_ && d == D_) return occupancy_t<true, NV_, TR_, D_>(smem);
-    LSK_IMPL_D(X, 1, 4) LSK_IMPL_D(X, 2, 2) LSK_IMPL_D(X, 4, 1)
-#undef X
-  }
   return 0;
 }
 
