@@ -196,7 +196,17 @@ def run_lsk(args):
         uid = [L.lsk_comm_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = L.lsk_comm_init(ws, rank, uid[0], local)
+        # in-kernel NVLink exchange: one persistent launch per GPU (NCCL multi-launch fallback)
+        exchange = "nccl-multilaunch"
+        if os.environ.get("LSK_P2P", "1") != "0":
+            try:
+                L.lsk_comm_enable_p2p(comm, synth.get_config(args.config).r)
+                exchange = "nvlink-p2p-in-kernel"
+            except L.LskError as e:
+                print("warning: peer exchange unavailable (%s); NCCL path" % e, file=sys.stderr)
 
+    if ws == 1:
+        exchange = "none"
     cfg = synth.get_config(args.config)
     variant = args.variant
     if variant == "auto":
@@ -251,6 +261,16 @@ def run_lsk(args):
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
+        if comm is not None:   # surface a cross-GPU exchange failure (the timed steps do not sync)
+            p = L.lsk_feature_params_init(eps, d, r, 0.0, cfg.anchor_seed, X, Y, comm=comm)
+            L.lsk_draw_anchors(p, U)
+            if var == "stream":
+                L.lsk_feature_map(p, U, X, Xi)
+                L.lsk_feature_map(p, U, Y, Ze)
+                L.lsk_factored_sinkhorn(Xi, Ze, a, b, eps, opts, u, v, report=True, comm=comm)
+            else:
+                L.lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, report=True,
+                                                 comm=comm)
         clocks = ClockSampler(local) if sample_clocks else None
         if dist is not None:
             dist.barrier()
@@ -321,6 +341,7 @@ def run_lsk(args):
         "config": {"workload": "config%d-%s" % (cfg.key, cfg.name), "variant": variant,
                    "n_per_gpu": cfg.n, "m_per_gpu": cfg.m, "d": d, "r": r, "eps": eps, "T": T,
                    "global_n": cfg.n * ws, "parallelism": "rows%d" % ws if ws > 1 else "single",
+                   "exchange": exchange,
                    "l2": "flushed (256 MiB write) before every timed step"},
         "roofline": main_m["roofline"],
         "kernel_ms": main_m["kernel_ms"],

@@ -284,6 +284,17 @@ lsk_status lsk_comm_get_unique_id(void* out_host);
 lsk_status lsk_comm_init(lsk_comm** out, int32_t nranks, int32_t rank,
                          const void* unique_id_host, int32_t device);
 lsk_status lsk_comm_destroy(lsk_comm* comm);
+/* Collective over the communicator's ranks (all must call it): map every rank's fp64 inbox
+ * ([2][nranks][~r_max + 6]) into every GPU's address space (CUDA IPC + peer access over
+ * NVLink; the handles travel in one NCCL all-gather).  Afterwards single-problem solves with
+ * this comm and r <= r_max run as ONE persistent launch per GPU: the per-half-iteration
+ * all-rank sum of the fp64 r-vector happens inside the kernel — the owner CTA of a column
+ * stores its rank's total into every peer's inbox and adds the N totals in rank order
+ * (deterministic, identical on every rank) — instead of one launch plus one ncclAllReduce per
+ * pass.  A peer that never arrives makes the solve fail after 20 s with LSK_ENCCL instead of
+ * hanging.  LSK_EUNSUPPORTED if peer memory cannot be mapped (the NCCL path stays in use);
+ * LSK_P2P=0 in the environment disables the in-kernel exchange.  Synchronises. */
+lsk_status lsk_comm_enable_p2p(lsk_comm* comm, int32_t r_max, void* stream);
 
 /* Number of kernels the library launched on this thread since the last reset (for the
  * bench's gpu_launches claim). */

@@ -128,6 +128,7 @@ _SIGS = {
     "lsk_comm_get_unique_id": (c_i32, [ctypes.c_void_p]),
     "lsk_comm_init": (c_i32, [P(ctypes.c_void_p), c_i32, c_i32, ctypes.c_void_p, c_i32]),
     "lsk_comm_destroy": (c_i32, [ctypes.c_void_p]),
+    "lsk_comm_enable_p2p": (c_i32, [ctypes.c_void_p, c_i32, ctypes.c_void_p]),
 }
 EXPORTED = sorted(_SIGS)
 for _name, (_res, _args) in _SIGS.items():
@@ -456,6 +457,12 @@ def lsk_comm_init(nranks: int, rank: int, unique_id: bytes, device: int):
 
 def lsk_comm_destroy(comm):
     _check(_lib.lsk_comm_destroy(comm), "lsk_comm_destroy")
+
+
+def lsk_comm_enable_p2p(comm, r_max: int, stream=None):
+    """Collective: map every rank's inbox over NVLink so that solves on `comm` run as one
+    persistent launch per GPU with the cross-GPU r-vector sum inside the kernel."""
+    _check(_lib.lsk_comm_enable_p2p(comm, int(r_max), _stream(stream)), "lsk_comm_enable_p2p")
 
 
 # ---------------------------------------------------------------- convenience -----------

@@ -108,6 +108,7 @@ struct NcclApi {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
 };
 static NcclApi& nccl() {
@@ -125,6 +126,7 @@ static NcclApi& nccl() {
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
     api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
   });
@@ -138,6 +140,10 @@ struct lsk_comm {
   int nranks = 1;
   int rank = 0;
   int device = 0;
+  // in-kernel NVLink exchange (lsk_comm_enable_p2p): every rank's inbox, own one allocated
+  bool p2p = false;
+  int xrs = 0;
+  double* xbox[lsk::kMaxRanks] = {};
 };
 
 namespace lsk {
@@ -306,11 +312,22 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   SolveCfg c;
   LSK_TRY(plan_solve(A, impl, batch, o, &c));
   if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  const bool p2p = comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
+                   !(getenv("LSK_P2P") && atoi(getenv("LSK_P2P")) == 0);
   if (comm && c.gpp < 2) {
-    // the multi-launch path needs svec: force >= 2 CTAs
+    // the cross-GPU paths reduce through svec: force >= 2 CTAs
     c.gpp = std::min(2, num_sms());
     c.grid = c.gpp;
     c.coop = true;
+  }
+  A.nranks = 1;
+  A.rank = 0;
+  if (p2p) {   // one persistent launch per GPU; the exchange runs over NVLink inside it
+    A.nranks = comm->nranks;
+    A.rank = comm->rank;
+    A.xrs = comm->xrs;
+    for (int i = 0; i < comm->nranks; ++i) A.xbox[i] = comm->xbox[i];
+    A.xtimeout_ns = 20LL * 1000 * 1000 * 1000;
   }
   A.gpp = c.gpp;
   A.dbg = getenv("LSK_DEBUG") ? atoi(getenv("LSK_DEBUG")) : 0;
@@ -335,7 +352,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 4 * (size_t)A.num_passes * c.gpp, s);
   }
   A.trace = trace;
-  if (!comm) {
+  if (!comm || p2p) {
     A.pass_begin = 0;
     A.pass_end = A.num_passes;
     A.multi_launch = 0;
@@ -383,7 +400,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       rp.iters = (int32_t)x[ST_ITERS];
       rp.converged = (int32_t)x[ST_CONV];
       rp.marginal_err = x[ST_ERR];
-      rp.rot = comm ? A.eps * (x[ST_FINAL_A] + x[ST_FINAL_B]) : x[ST_ROT];
+      rp.rot = (comm && !p2p) ? A.eps * (x[ST_FINAL_A] + x[ST_FINAL_B]) : x[ST_ROT];
       rp.sum_a_log_u = x[ST_FINAL_A];
       rp.sum_b_log_v = x[ST_FINAL_B];
       rp.breakdown = x[ST_BRK] > 0 ? 1 : 0;
@@ -391,6 +408,9 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       brk |= rp.breakdown != 0;
       notconv |= A.tol_mode && !rp.converged;
     }
+    for (int b = 0; b < batch; ++b)
+      if (st[(size_t)b * kStateDoubles + ST_XERR] != 0.0)
+        return fail(LSK_ENCCL, "cross-GPU peer exchange timed out (a rank did not arrive)");
     if (brk) return fail(LSK_EBREAKDOWN, "zero or non-finite row dot during Sinkhorn");
     if (notconv) {
       g_err = "tolerance not reached within max_iters";
@@ -1045,9 +1065,70 @@ lsk_status lsk_comm_init(lsk_comm** out, int32_t nranks, int32_t rank,
   return LSK_OK;
 }
 
+lsk_status lsk_comm_enable_p2p(lsk_comm* c, int32_t r_max, void* stream) {
+  if (!c || r_max < 4) return fail(LSK_EINVAL, "bad arguments");
+  if (c->nranks > kMaxRanks) return fail(LSK_EUNSUPPORTED, "more ranks than kMaxRanks");
+  if (!nccl().ok || !nccl().allGather) return fail(LSK_ENCCL, "NCCL (allGather) not loadable");
+  if (c->p2p) return LSK_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LSK_CU(cudaSetDevice(c->device));
+  const int N = c->nranks;
+  const int xrs = ((r_max + kExtra + 2) + 31) & ~31;
+  double* mine = nullptr;
+  LSK_CU(cudaMalloc(&mine, sizeof(double) * 2 * N * xrs));
+  LSK_CU(cudaMemset(mine, 0xFF, sizeof(double) * 2 * N * xrs));   // all-ones sentinel
+  LSK_CU(cudaDeviceSynchronize());
+  // exchange the IPC handles with one NCCL all-gather (it also orders every rank's sentinel
+  // initialisation before any peer store: no rank starts a solve before the gather completes)
+  cudaIpcMemHandle_t h;
+  LSK_CU(cudaIpcGetMemHandle(&h, mine));
+  char* dbuf = nullptr;
+  LSK_CU(cudaMalloc(&dbuf, sizeof(h) * (N + 1)));
+  LSK_CU(cudaMemcpyAsync(dbuf + sizeof(h) * N, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  lsk_status st = nccl_check(nccl().allGather(dbuf + sizeof(h) * N, dbuf, sizeof(h), ncclChar,
+                                              c->comm, s), "ncclAllGather(ipc handles)");
+  std::vector<cudaIpcMemHandle_t> all(N);
+  if (st == LSK_OK) {
+    LSK_CU(cudaMemcpyAsync(all.data(), dbuf, sizeof(h) * N, cudaMemcpyDeviceToHost, s));
+    LSK_CU(cudaStreamSynchronize(s));
+  }
+  cudaFree(dbuf);
+  if (st != LSK_OK) {
+    cudaFree(mine);
+    return st;
+  }
+  for (int i = 0; i < N; ++i) {
+    if (i == c->rank) {
+      c->xbox[i] = mine;
+      continue;
+    }
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[i], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < i; ++j)
+        if (j != c->rank && c->xbox[j]) cudaIpcCloseMemHandle(c->xbox[j]);
+      cudaFree(mine);
+      for (auto& x : c->xbox) x = nullptr;
+      return fail(LSK_EUNSUPPORTED, std::string("peer memory unavailable: ") + cudaGetErrorString(e));
+    }
+    c->xbox[i] = static_cast<double*>(ptr);
+  }
+  c->xrs = xrs;
+  c->p2p = true;
+  return LSK_OK;
+}
+
 lsk_status lsk_comm_destroy(lsk_comm* comm) {
   if (!comm) return LSK_OK;
   lsk_status st = LSK_OK;
+  if (comm->p2p) {
+    for (int i = 0; i < comm->nranks; ++i) {
+      if (!comm->xbox[i]) continue;
+      if (i == comm->rank) cudaFree(comm->xbox[i]);
+      else cudaIpcCloseMemHandle(comm->xbox[i]);
+    }
+  }
   if (comm->comm) st = nccl_check(nccl().commDestroy(comm->comm), "ncclCommDestroy");
   delete comm;
   return st;

@@ -12,6 +12,7 @@ constexpr int kThreads = kConsumerThreads + 32;    // + 1 producer warp
 constexpr int kExtra = 4;                          // extras appended to every r-vector:
                                                    // [0]=err, [1]=breakdown, [2..3]=0
 constexpr int kStateDoubles = 16;                  // per-problem solve state block
+constexpr int kMaxRanks = 8;                       // GPUs of one node in the peer exchange
 // state block layout (doubles)
 enum StateIdx {
   ST_ERR = 3,      // latest marginal error
@@ -21,7 +22,8 @@ enum StateIdx {
   ST_CONV = 7,     // converged flag
   ST_BRK = 8,      // breakdown count
   ST_FINAL_A = 9,  // a^T log u of the returned state
-  ST_FINAL_B = 10  // b^T log v of the returned state
+  ST_FINAL_B = 10, // b^T log v of the returned state
+  ST_XERR = 11     // 1 if a cross-GPU peer exchange timed out
 };
 
 // Pass schedule: p = 0 init xi-pass (s_v = xi^T 1), p = 2t-1 v-pass of iteration t,
@@ -70,6 +72,13 @@ struct SinkArgs {
   float l2_resident;       // fraction of each CTA's rows per factor kept L2-resident (evict_last)
   int tr;                  // rows per tile (template dispatch)
   int nv;                  // float4 column groups per consumer thread (template dispatch)
+  // cross-GPU exchange inside the persistent launch (nranks > 1; lsk_sink_common.cuh):
+  // every rank's inbox [2 parity][nranks source][xrs] fp64, mapped over NVLink (peer memory)
+  int nranks;
+  int rank;
+  int xrs;
+  double* xbox[kMaxRanks];
+  long long xtimeout_ns;   // a peer poll gives up after this long (ST_XERR, no hang)
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.

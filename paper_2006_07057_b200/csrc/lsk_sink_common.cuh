@@ -98,8 +98,52 @@ __device__ __forceinline__ double2 sv_load2(const double* p, bool multi) {
   return make_double2(__longlong_as_double((long long)b0), __longlong_as_double((long long)b1));
 }
 
-// R2 owner: publish column k of pass p and re-arm the same column of pass p-1's buffer
+// ---- cross-GPU exchange over NVLink peer memory (one persistent launch per GPU) -----------
+// The owner of column k on every rank (same CTA partition on every rank) adds the ranks' local
+// totals in rank order: it stores its own total into slot [par][my rank][k] of EVERY rank's
+// inbox (st.release.sys through NVLink), polls its own inbox slots [par][src][k] until they
+// differ from the all-ones sentinel (ld.acquire.sys), sums them src = 0, 1, ... (the same bits
+// on every rank: deterministic), and re-arms the slots it consumed.  par alternates with the
+// pass: ranks can be at most one pass apart (pass p+1 needs every rank's pass-p totals), and a
+// slot consumed in pass p is rewritten in pass p+2 only after its source saw this rank's pass
+// p+1 total — which this thread stores after the re-arm (release/acquire causality).  A poll
+// that outlives A.xtimeout_ns sets ST_XERR and yields NaN, so a broken peer cannot hang the GPU.
+__device__ __forceinline__ double xpoll(const double* p, long long deadline, int* timed_out) {
+  unsigned long long b;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+    if (b != kSvSentinel) return __longlong_as_double((long long)b);
+    if (*timed_out || (long long)globaltimer() > deadline) {
+      *timed_out = 1;
+      return __longlong_as_double(0x7ff8000000000000ll);   // NaN
+    }
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ double xrank_total(const SinkArgs& A, int prob, int par, int k,
+                                              double local) {
+  const int N = A.nranks;
+  for (int d = 0; d < N; ++d)
+    asm volatile("st.release.sys.global.f64 [%0], %1;" ::"l"(A.xbox[d] + ((int64_t)(par * N + A.rank) * A.xrs + k)),
+                 "d"(local)
+                 : "memory");
+  double* mine = A.xbox[A.rank] + (int64_t)par * N * A.xrs + k;
+  const long long deadline = (long long)globaltimer() + A.xtimeout_ns;
+  int timed_out = 0;
+  double tot = 0.0;
+  for (int src = 0; src < N; ++src) tot += xpoll(mine + (int64_t)src * A.xrs, deadline, &timed_out);
+  for (int src = 0; src < N; ++src)
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(mine + (int64_t)src * A.xrs), "l"(kSvSentinel)
+                 : "memory");
+  if (timed_out) A.state[(int64_t)prob * kStateDoubles + ST_XERR] = 1.0;
+  return tot;
+}
+
+// R2 owner: publish column k of pass p (the all-rank total when the launch spans GPUs) and
+// re-arm the same column of pass p-1's buffer
 __device__ __forceinline__ void sv_publish(const SinkArgs& A, int prob, int pass, int k, double v) {
+  if (A.nranks > 1) v = xrank_total(A, prob, pass & 1, k, v);
   double* cur = sv_of(A, prob, pass);
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(cur + k), "d"(v) : "memory");
   if (!A.multi_launch) {

@@ -493,6 +493,10 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       }
     }
     if (cta == 0 && tid == 0) {
+      if (A.nranks > 1) {   // all-rank read-out: columns r+kExtra, r+kExtra+1 of parity 0
+        la = xrank_total(A, prob, 0, (int)rstride, la);
+        lb = xrank_total(A, prob, 0, (int)rstride + 1, lb);
+      }
       stg_state[ST_ITERS] = (double)final_t;
       stg_state[ST_FINAL_A] = la;
       stg_state[ST_FINAL_B] = lb;

@@ -2,7 +2,12 @@
 multi-GPU solver — rows partitioned by the library's lsk_shard_range, one fp64 all-reduce
 of the r-vector partial per half-iteration, all-reduced read-out — with the oracle's
 arithmetic standing in for the local GPU pass.  The gathered result must equal the
-unsharded oracle solve (same fp64 math, only the summation split differs)."""
+unsharded oracle solve (same fp64 math, only the summation split differs).
+
+exchange="rank_order" models the in-kernel NVLink exchange (lsk_comm_enable_p2p): every rank
+receives every rank's fp64 partial (the peer inboxes; here an all-gather) and adds them in
+rank order starting from 0.0 — every rank must end with bit-identical vectors, and so with
+identical stopping decisions and read-out."""
 import os
 import socket
 
@@ -23,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, ws, port, T, q):
+def _worker(rank, ws, port, T, q, exchange="allreduce"):
     import sys
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -48,9 +53,17 @@ def _worker(rank, ws, port, T, q):
     b = prob["b"][mb:me].astype(np.float64)
 
     def allreduce(x):
-        t = torch.from_numpy(np.ascontiguousarray(x))
-        dist.all_reduce(t)
-        return t.numpy()
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if exchange == "allreduce":
+            t = torch.from_numpy(x.copy())
+            dist.all_reduce(t)
+            return t.numpy()
+        parts = [torch.zeros_like(torch.from_numpy(x)) for _ in range(ws)]
+        dist.all_gather(parts, torch.from_numpy(x))       # every rank's inbox slots
+        tot = np.zeros_like(x)
+        for src in range(ws):                            # rank order, from 0.0
+            tot = tot + parts[src].numpy()
+        return tot
 
     s_v = allreduce(xi @ np.ones(ne - nb))           # init pass: xi^T 1
     for _ in range(T):
@@ -62,25 +75,28 @@ def _worker(rank, ws, port, T, q):
     rot = cfg.eps * parts.sum()
     us = [None] * ws
     vs = [None] * ws
+    rots = [None] * ws
     dist.all_gather_object(us, u)
     dist.all_gather_object(vs, v)
+    dist.all_gather_object(rots, rot)
     if rank == 0:
-        q.put((rot, np.concatenate(us), np.concatenate(vs), float(Rl)))
+        q.put((rot, np.concatenate(us), np.concatenate(vs), float(Rl), rots))
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", ["allreduce", "rank_order"])
 @pytest.mark.parametrize("ws", [2])
-def test_row_sharded_protocol_matches_unsharded(ws):
+def test_row_sharded_protocol_matches_unsharded(ws, exchange):
     import oracle as O
     import synth
     T = 25
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(k, ws, port, T, q)) for k in range(ws)]
+    procs = [ctx.Process(target=_worker, args=(k, ws, port, T, q, exchange)) for k in range(ws)]
     for p in procs:
         p.start()
-    rot, u, v, R = q.get(timeout=300)
+    rot, u, v, R, rots = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -90,3 +106,5 @@ def test_row_sharded_protocol_matches_unsharded(ws):
     ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, 64, cfg.anchor_seed, T=T)
     assert abs(rot - ref["rot"]) <= 1e-12 * abs(ref["rot"])
     assert np.allclose(u, ref["u"], rtol=1e-11) and np.allclose(v, ref["v"], rtol=1e-11)
+    if exchange == "rank_order":
+        assert all(x == rots[0] for x in rots)           # bit-identical on every rank

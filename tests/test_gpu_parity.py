@@ -356,6 +356,36 @@ def test_nccl_multilaunch_one_rank(L, variant):
         L.lsk_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
+def test_p2p_exchange_one_rank(L, variant):
+    """The in-kernel cross-GPU exchange (lsk_comm_enable_p2p: one persistent launch per GPU,
+    every column's all-rank total formed by its owner CTA through the peer inboxes) on one GPU
+    with a 1-rank communicator: the whole protocol runs (store to every inbox, sentinel polls,
+    rank-order sum, re-arm) and, with one rank, the total is 0.0 + local — so u, v and W_hat are
+    bit-identical to the single-GPU launch, in fixed-T and tolerance mode, solve after solve."""
+    import torch
+    uid = L.lsk_comm_get_unique_id()
+    comm = L.lsk_comm_init(1, 0, uid, torch.cuda.current_device())
+    try:
+        L.lsk_comm_enable_p2p(comm, 1024)
+        cfg = synth.get_config(2)
+        prob = synth.make_problem(cfg, n=3001, m=2999)
+        X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+        for T in (40, 41):   # both parities of the last pass
+            res = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T, variant=variant,
+                        comm=comm)
+            single = _run_gpu(L, prob, T, variant=variant)
+            assert torch.equal(res["u"], single["u"]) and torch.equal(res["v"], single["v"])
+            assert res["rot"] == single["rot"]
+        res_t = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, max_iters=300, tol=1e-4,
+                      variant=variant, comm=comm)
+        single_t = _run_gpu(L, prob, 300, variant=variant, tol=1e-4)
+        assert res_t["report"]["iters"] == single_t["report"]["iters"]
+        assert res_t["rot"] == single_t["rot"]
+    finally:
+        L.lsk_comm_destroy(comm)
+
+
 def test_smoke_entry_point(L):
     import importlib, sys, os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
