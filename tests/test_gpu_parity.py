@@ -273,6 +273,51 @@ def test_single_point_and_tiny(L):
         _check_parity(_run_gpu(L, prob, 40, variant=variant), ref)
 
 
+@pytest.mark.parametrize("variant,d,r", [("stream", 2, 8192), ("implicit", 8, 4096),
+                                         ("implicit", 3, 4096), ("stream", 16, 2048)])
+def test_largest_supported_shapes(L, variant, d, r):
+    """The largest r each kernel instantiates (stream: 8 float4 groups per consumer thread,
+    r = 8192; implicit: r = 4096 at the largest d = 8 and at d = 3) on a ragged small n."""
+    rng = np.random.default_rng(11)
+    n, m = 1031, 997
+    x = rng.normal(0.0, 0.3, size=(n, d))
+    y = rng.normal(0.2, 0.3, size=(m, d))
+    a = rng.uniform(0.5, 1.5, n); a /= a.sum()
+    b = rng.uniform(0.5, 1.5, m); b /= b.sum()
+    prob = dict(X=x.astype(np.float32), Y=y.astype(np.float32), a=a.astype(np.float32),
+                b=b.astype(np.float32), eps=0.5, r=r, seed=13)
+    T = 30
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], 0.5, r, 13, T=T)
+    _check_parity(_run_gpu(L, prob, T, variant=variant), ref)
+
+
+def test_invalid_arguments_fail_loudly(L):
+    """Empty inputs, r not a multiple of 4, eps <= 0 and d beyond a kernel's range are
+    rejected with the documented status codes (no silent fallback)."""
+    import torch
+    X = torch.zeros((0, 2), device="cuda")
+    Y = torch.zeros((5, 2), device="cuda")
+    a = torch.ones(0, device="cuda")
+    b = torch.ones(5, device="cuda") / 5
+    with pytest.raises(L.LskError) as e:
+        L.rot(X, Y, a, b, 0.5, 8, 1, iters=3)
+    assert e.value.status in (-1,)
+    Xn = torch.rand((4, 2), device="cuda")
+    an = torch.ones(4, device="cuda") / 4
+    for r in (6, 0):
+        with pytest.raises(L.LskError) as e:
+            L.rot(Xn, Y, an, b, 0.5, r, 1, iters=3)
+        assert e.value.status == -1
+    with pytest.raises(L.LskError) as e:
+        L.rot(Xn, Y, an, b, -1.0, 8, 1, iters=3)
+    assert e.value.status == -1
+    X9 = torch.rand((4, 9), device="cuda") * 0.1
+    Y9 = torch.rand((5, 9), device="cuda") * 0.1
+    with pytest.raises(L.LskError) as e:
+        L.rot(X9, Y9, an, b, 0.5, 8, 1, iters=3, variant="implicit")
+    assert e.value.status == -2   # LSK_EDIM: the implicit kernels take d <= 8
+
+
 def test_rank_one_full_size_closed_form(L):
     """Config 5 at FULL size with identical points: K_theta = kappa 11^T, so one loop gives
     W = eps(sum a ln a + sum b ln b - (sum b) ln kappa + (sum a - sum b) ln n
