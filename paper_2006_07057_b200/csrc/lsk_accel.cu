@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) lam_kernel(double tau, AccelVecs v) 
 // <= 32 rows per warp, then fp64; warps combined in a fixed order).  One warp per row pair:
 // lane l holds float4 column groups {l, l+32, ...} (coalesced 512-byte loads per group).
 template <int NV, int ROWS>
-__global__ void __launch_bounds__(kThreads, NV <= 8 ? 2 : 1) pass_kernel(const float* __restrict__ F,
+__global__ void __launch_bounds__(kThreads, 1) pass_kernel(const float* __restrict__ F,
                                                         int64_t rows, int r,
                                                         const double* __restrict__ s_in,
                                                         const double* __restrict__ lam,
@@ -403,10 +403,11 @@ __global__ void __launch_bounds__(kThreads) normalise_kernel(const float* a, con
 }  // namespace accel
 
 // ------------------------------------------------------------------------------ launchers
-// vector kernels: one CTA per SM per block side; factor passes: two CTAs per SM (loads in
-// flight), partials reduced by reduce_kernel
+// vector kernels: one CTA per SM per block side; factor passes: one CTA per SM with up to
+// 255 registers (four rows of 4 KB in flight per warp at r = 1000), partials reduced by
+// reduce_kernel
 int accel_grid() { return 148; }
-int accel_pass_grid() { return 296; }
+int accel_pass_grid() { return 148; }
 
 cudaError_t launch_accel_normalise(const float* a, const float* b, const AccelVecs& v,
                                    cudaStream_t s) {
@@ -425,7 +426,7 @@ template <int NV>
 static cudaError_t pass_nv(const float* F, int64_t rows, int r, const double* s_in,
                            const double* lam, const double* Mp, double* t_out, double* part,
                            cudaStream_t s) {
-  constexpr int ROWS = NV <= 8 ? 2 : 1;
+  constexpr int ROWS = NV <= 4 ? 8 : NV <= 8 ? 4 : 1;   // rows in flight per warp
   const int G = accel_pass_grid();
   auto kern = accel::pass_kernel<NV, ROWS>;
   const size_t dyn = lam ? sizeof(double) * accel::kWarps * NV * 4 * 32 : 0;
