@@ -74,8 +74,15 @@ typedef struct lsk_solve_opts {
   int32_t want_marginal_err;
   double tol;
   int32_t ctas_per_sm;     /* 0 = library default                                         */
-  int32_t reserved;
+  int32_t flags;           /* LSK_SOLVE_STABILIZE: implicit solver in the row-normalised form */
 } lsk_solve_opts;
+
+/* flags of lsk_solve_opts.  LSK_SOLVE_STABILIZE (lsk_factored_sinkhorn_implicit only; reading
+ * C30): every row of the regenerated factors is normalised by its largest entry (a per-row
+ * shift of the exponent), so no row underflows fp32 at small eps; u, v are then the scalings
+ * u~ = u e^A, v~ = v e^B of the normalised problem (lsk_implicit_row_offsets returns A, B) and
+ * rep->rot is the value of the original problem (the offsets are folded in). */
+#define LSK_SOLVE_STABILIZE 1
 
 /* Report of one solve.  rot = W_hat of the returned (u, v);
  * marginal_err = |v o K^T u - b|_1 of the returned state, or -1 if not evaluated. */
@@ -211,6 +218,10 @@ lsk_status lsk_rot_gradient(const lsk_feature_params* p, const float* U, const f
                             float* gY, float* gU, void* stream);
 
 /* ---- NEXT f4: small-eps stabilisation (reading C30) ------------------------ */
+/* The fp64 row offsets A_i = ln max_k xi_ik of the stabilised implicit solver (same arithmetic
+ * as inside it): u = u~ e^{-A}.  logoff: device fp64 (n).  d <= 8.  Asynchronous. */
+lsk_status lsk_implicit_row_offsets(const lsk_feature_params* p, const float* U, const float* X,
+                                    int64_t n, double* logoff, void* stream);
 /* Row-normalised Gaussian features: Xi (n x r) = xi / max_k xi_k (every row's largest entry
  * is 1, so no row underflows fp32 at small eps) and logoff (n, fp64) = A_i = ln max_k xi_ik,
  * i.e. xi = diag(e^A) Xi.  Alg. 1 on (Xi_x, Xi_y) returns u~ = u e^A, v~ = v e^B (it starts

@@ -41,7 +41,7 @@ class lsk_feature_params(ctypes.Structure):
 
 class lsk_solve_opts(ctypes.Structure):
     _fields_ = [("max_iters", c_i32), ("want_marginal_err", c_i32), ("tol", ctypes.c_double),
-                ("ctas_per_sm", c_i32), ("reserved", c_i32)]
+                ("ctas_per_sm", c_i32), ("flags", c_i32)]
 
 
 class lsk_report(ctypes.Structure):
@@ -111,6 +111,8 @@ _SIGS = {
     "lsk_rot_gradient": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p, c_i64,
                                  c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p, c_f32p,
                                  ctypes.c_void_p]),
+    "lsk_implicit_row_offsets": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64,
+                                         ctypes.c_void_p, ctypes.c_void_p]),
     "lsk_feature_map_stabilized": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p, c_i64, c_f32p,
                                            ctypes.c_void_p, ctypes.c_void_p]),
     "lsk_rot_value_offset": (c_i32, [c_f32p, c_f32p, c_f32p, c_f32p, ctypes.c_void_p,
@@ -193,9 +195,13 @@ def _stream(stream=None) -> int:
     return stream.cuda_stream
 
 
+LSK_SOLVE_STABILIZE = 1
+
+
 def make_opts(iters: int, tol: float = 0.0, want_err: bool = False,
-              ctas_per_sm: int = 0) -> lsk_solve_opts:
-    return lsk_solve_opts(int(iters), 1 if want_err else 0, float(tol), int(ctas_per_sm), 0)
+              ctas_per_sm: int = 0, stabilize: bool = False) -> lsk_solve_opts:
+    return lsk_solve_opts(int(iters), 1 if want_err else 0, float(tol), int(ctas_per_sm),
+                          LSK_SOLVE_STABILIZE if stabilize else 0)
 
 
 # ---------------------------------------------------------------- C-ABI mirrors ----------
@@ -349,6 +355,12 @@ def lsk_feature_map_stabilized(p, U, X, Xi, logoff, stream=None):
            "lsk_feature_map_stabilized")
 
 
+def lsk_implicit_row_offsets(p, U, X, logoff, stream=None):
+    """fp64 row offsets A (n) of the stabilised implicit solver: u = u~ e^{-A}."""
+    _check(_lib.lsk_implicit_row_offsets(ctypes.byref(p), _f32(U), _f32(X), X.shape[0],
+                                         _ptr(logoff), _stream(stream)), "lsk_implicit_row_offsets")
+
+
 def lsk_rot_value_offset(u, v, a, b, A, B, eps, stream=None) -> float:
     out = ctypes.c_double()
     _check(_lib.lsk_rot_value_offset(_f32(u), _f32(v), _f32(a), _f32(b), _ptr(A), _ptr(B),
@@ -470,8 +482,9 @@ def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
         want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None, stabilize=False):
     """Whole hot path on device tensors: a1 params -> a2 anchors -> a3 features -> Alg. 1 ->
     a9 read-out.  variant: "stream" (materialise xi, zeta) or "implicit" (recompute).
-    stabilize=True (stream, d <= 16): row-normalised features with log offsets (reading C30);
-    u, v are then the scalings of the normalised problem and A, B the offsets."""
+    stabilize=True: row-normalised features with log offsets (reading C30; stream: d <= 16,
+    implicit: d <= 8); u, v are then the scalings of the normalised problem and A, B the
+    offsets."""
     import torch
     dev = X.device
     d = X.shape[1]
@@ -482,11 +495,17 @@ def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
     u = torch.empty(n, dtype=torch.float32, device=dev)
     v = torch.empty(m, dtype=torch.float32, device=dev)
     T = iters if iters is not None else (max_iters or 1000)
-    opts = make_opts(T, tol, want_err, ctas_per_sm)
+    opts = make_opts(T, tol, want_err, ctas_per_sm, stabilize=stabilize and variant == "implicit")
     out = dict(params=p.as_dict(), U=U, u=u, v=v)
     if variant == "implicit":
         rep = lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, comm=comm,
                                              stream=stream)
+        if stabilize:
+            A = torch.empty(n, dtype=torch.float64, device=dev)
+            B = torch.empty(m, dtype=torch.float64, device=dev)
+            lsk_implicit_row_offsets(p, U, X, A, stream)
+            lsk_implicit_row_offsets(p, U, Y, B, stream)
+            out.update(A=A, B=B)
     else:
         Xi = torch.empty((n, r), dtype=torch.float32, device=dev)
         Zeta = torch.empty((m, r), dtype=torch.float32, device=dev)

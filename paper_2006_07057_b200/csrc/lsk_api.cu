@@ -664,10 +664,15 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   if (!U || !X || !Y || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
   if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool stab = (o && (o->flags & LSK_SOLVE_STABILIZE));
+  if (stab && comm) return fail(LSK_EUNSUPPORTED, "the stabilised implicit solve is single-GPU");
   char* ws;
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
+  const size_t oM = stab ? cv.take(sizeof(float) * (n + m)) : 0;    // row shifts m_j
+  const size_t oA = stab ? cv.take(sizeof(double) * (n + m)) : 0;   // row offsets A_j
+  const size_t oR = stab ? cv.take(16384) : 0;                      // read-out scratch
   LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms(), n), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
@@ -680,8 +685,50 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   A.r = p->r; A.d = p->d; A.eps = p->eps;
   A.Wt = Wt; A.beta2 = b2;
   A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
-  LSK_TRY(setup_fact(A, p->R, 1, s, ws, cv));
-  return run_solve(A, true, 1, o, rep, comm, s, ws, cv);
+  double* offs = nullptr;
+  if (stab) {   // reading C30: per-row shifts inside the kernel, offsets folded into the read-out
+    float* m2 = reinterpret_cast<float*>(ws + oM);
+    offs = reinterpret_cast<double*>(ws + oA);
+    LSK_CU(launch_row_shift(X, n, p->d, Wt, b2, p->r, A.c2, m2, offs, s));
+    LSK_CU(launch_row_shift(Y, m, p->d, Wt, b2, p->r, A.c2, m2 + n, offs + n, s));
+    A.hrow[0] = m2;
+    A.hrow[1] = m2 + n;
+    A.stab = 1;
+  } else {
+    LSK_TRY(setup_fact(A, p->R, 1, s, ws, cv));
+  }
+  lsk_status st = run_solve(A, true, 1, o, rep, comm, s, ws, cv);
+  if (stab && rep && st >= 0) {
+    double* scratch = reinterpret_cast<double*>(ws + oR);
+    LSK_CU(launch_rot_value(u, v, a, b, n, m, 1, scratch + 32, scratch, s, offs, offs + n));
+    double h[2];
+    LSK_CU(cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, s));
+    LSK_CU(cudaStreamSynchronize(s));
+    rep->sum_a_log_u = h[0];
+    rep->sum_b_log_v = h[1];
+    rep->rot = p->eps * (h[0] + h[1]);
+  }
+  return st;
+}
+
+lsk_status lsk_implicit_row_offsets(const lsk_feature_params* p, const float* U, const float* X,
+                                    int64_t n, double* logoff, void* stream) {
+  if (!p || !U || !X || !logoff) return fail(LSK_EINVAL, "NULL argument");
+  if (n < 1 || p->r < 4 || p->r % 4) return fail(LSK_EINVAL, "bad sizes");
+  if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  const size_t oM = cv.take(sizeof(float) * n);
+  LSK_TRY(get_ws(s, cv.off, &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  LSK_CU(launch_row_shift(X, n, p->d, Wt, b2, p->r, (float)(-2.0 * 1.4426950408889634074 / p->eps),
+                          reinterpret_cast<float*>(ws + oM), logoff, s));
+  return LSK_OK;
 }
 
 lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float* Zeta,

@@ -72,8 +72,11 @@ struct Smem {
   int ist[2];                      // final_t, conv
 };
 
-template <int TS, int TEAMS, int NV, int TR, int D, bool FACT, bool PIPE>
+// MODE 0: expanded exponent; 1: factored (row factor h_j); 2: stabilised (per-row shift m_j,
+// scalings of the row-normalised problem, reading C30)
+template <int TS, int TEAMS, int NV, int TR, int D, int MODE, bool PIPE>
 __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs A) {
+  constexpr bool FACT = MODE == 1, STAB = MODE == 2;
   constexpr int NT = TS * TEAMS;       // CTA threads
   constexpr int NWT = TS / 32;         // warps per team
   constexpr int NW = NT / 32;
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     const int ntiles = (ntiles_cta - team + TEAMS - 1) / TEAMS;   // this team: tiles team, team+TEAMS, ...
     const float* wp0 = A.w[f] + (int64_t)prob * A.wstride[f] + r0;
     const float* Xp0 = A.X[f] + (int64_t)prob * A.fstride[f] + r0 * D;
-    const float* hp0 = FACT ? A.hrow[f] + (int64_t)prob * A.wstride[f] + r0 : nullptr;
+    const float* hp0 = (FACT || STAB) ? A.hrow[f] + (int64_t)prob * A.wstride[f] + r0 : nullptr;
     const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
     const float* vold0 =
         need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) + r0 : nullptr;
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
         float* sl = tslots + (gi % kRing) * SLOT;
         if (lane < TR && lane < nrows - lr) {
           cp_async4(sl + lane, wp0 + lr + lane);
-          if (FACT) cp_async4(sl + 32 + lane, hp0 + lr + lane);
+          if (FACT || STAB) cp_async4(sl + 32 + lane, hp0 + lr + lane);
           if (need_vold) cp_async4(sl + 64 + lane, vold0 + lr + lane);
 #pragma unroll
           for (int c = 0; c < D; ++c) cp_async4(sl + 96 + lane * XS + c, Xp0 + (lr + lane) * D + c);
@@ -320,7 +323,10 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
             }
           }
           float2 al2 = make_float2(0.f, 0.f);
-          if constexpr (!FACT) {
+          if constexpr (STAB) {
+            const float mj = -sl[32 + i];   // the row's shift: every G_jk <= ~1
+            al2 = make_float2(mj, mj);
+          } else if constexpr (!FACT) {
             float al = 0.f;
 #pragma unroll
             for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           for (int j = 0; j < NV; ++j) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);
+              float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);   // STAB: al2 = -m_j
 #pragma unroll
               for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
               fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           if (valid) {
             const float c = sl[row];
             const float h = FACT ? sl[32 + row] : 1.f;
-            const float tj = FACT ? h * tot : tot;     // t_j = F_j . s
+            const float tj = FACT ? h * tot : tot;     // t_j = F_j . s (STAB: of the normalised K)
             const float w = c * rcp_approx(tj);        // w_j = c_j / t_j
             wt = FACT ? w * h : w;
             if (twarp == NWT - 1 && (lane % G) == 0) {   // outputs: one lane per row
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           }
           if constexpr (!kAcc) wt = 0.f;
         } else {
-          if (valid) wt = FACT ? sl[32 + row] : 1.f;   // u^0 = 1 (reading C6): w~ = h
+          if (valid) wt = FACT ? sl[32 + row] : 1.f;   // u^0 = 1 (reading C6): w~ = h; STAB: u~^0 = 1
         }
         if constexpr (kAcc) {
 #pragma unroll
@@ -627,6 +633,40 @@ __global__ void row_scale_kernel(const float* __restrict__ X, int64_t n, float c
   h[j] = ex2(al * c2 - abar);
 }
 
+// Stabilised mode (reading C30): m_j = max_k (beta2_k + sum_c W_kc p_jc) (log2 units, the same
+// fp32 FMA order as the kernel's exponent) and the fp64 natural-log row offset
+// A_j = (alpha2_j + m_j) ln 2 with alpha2_j = c2 |p_j|^2, so F_jk = e^{A_j} 2^{beta2_k + W_k.p_j - m_j}.
+// Anchor constants staged in shared memory; one thread per row.
+template <int D>
+__global__ void __launch_bounds__(256) row_shift_kernel(const float* __restrict__ X, int64_t n,
+                                                        const float* __restrict__ Wt,
+                                                        const float* __restrict__ beta2, int r,
+                                                        float c2, float* __restrict__ m2,
+                                                        double* __restrict__ A) {
+  extern __shared__ float cst[];   // [D + 1][r]: W rows, then beta2
+  for (int i = threadIdx.x; i < (D + 1) * r; i += blockDim.x)
+    cst[i] = i < D * r ? Wt[i] : beta2[i - D * r];
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float x[D];
+  float al = 0.f;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    x[c] = X[j * D + c];
+    al = fmaf(x[c], x[c], al);
+  }
+  float mx = -INFINITY;
+  for (int k = 0; k < r; ++k) {
+    float e = cst[D * r + k];
+#pragma unroll
+    for (int c = 0; c < D; ++c) e = fmaf(cst[c * r + k], x[c], e);
+    mx = fmaxf(mx, e);
+  }
+  m2[j] = mx;
+  A[j] = ((double)(al * c2) + (double)mx) * 0.69314718055994530942;
+}
+
 template <int TS, int TEAMS, int NV, int TR, int D>
 constexpr size_t dyn_smem() {
   return sizeof(double) * NV * 4 * TS * TEAMS + sizeof(float) * TEAMS * kRing * Geo<D>::SLOT +
@@ -681,9 +721,9 @@ ImplCfg implicit_config(int r, int d) {
   LSK_IMPL_D123(X, 256, 1, 4, 8, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                  \
   LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2)
 
-template <int TS, int TM, int NV, int TR, int D, bool FACT, bool PIPE>
+template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
-  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, FACT, PIPE>;
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE>;
   constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
@@ -698,9 +738,9 @@ static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream
   return e;
 }
 
-template <int TS, int TM, int NV, int TR, int D, bool FACT, bool PIPE>
+template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE>
 static int occupancy_cfg() {
-  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, FACT, PIPE>;
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE>;
   constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
   int nb = 0;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -708,14 +748,31 @@ static int occupancy_cfg() {
   return nb;
 }
 
+// the stabilised mode is instantiated for the default (non-pipelined) configurations only
+template <int TS, int TM, int NV, int TR, int D, int P>
+static cudaError_t stab_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s, int* occ) {
+  if constexpr (P == 0 && !(TS == 128 && TM == 3)) {
+    if (occ) {
+      *occ = occupancy_cfg<TS, TM, NV, TR, D, 2, false>();
+      return cudaSuccess;
+    }
+    return launch_cfg<TS, TM, NV, TR, D, 2, false>(a, coop, grid, s);
+  } else {
+    return cudaErrorInvalidConfiguration;
+  }
+}
+
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
   const ImplCfg c = implicit_config(a.r, a.d);
+  if (c.warp && a.stab) return cudaErrorInvalidConfiguration;   // team kernel only
   if (c.warp) return launch_implicit_warp(a, coop, grid, s, nullptr);
-  const bool fact = a.hrow[0] != nullptr;
+  const int mode = a.stab ? 2 : (a.hrow[0] != nullptr ? 1 : 0);
 #define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
-  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) \
-    return fact ? launch_cfg<TS_, TM_, NV_, TR_, D_, true, P_>(a, coop, grid, s)               \
-                : launch_cfg<TS_, TM_, NV_, TR_, D_, false, P_>(a, coop, grid, s);
+  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) { \
+    if (mode == 2) return stab_cfg<TS_, TM_, NV_, TR_, D_, P_>(a, coop, grid, s, nullptr);       \
+    return mode == 1 ? launch_cfg<TS_, TM_, NV_, TR_, D_, 1, P_>(a, coop, grid, s)             \
+                     : launch_cfg<TS_, TM_, NV_, TR_, D_, 0, P_>(a, coop, grid, s);            \
+  }
   LSK_IMPL_ALL(X)
 #undef X
   return cudaErrorInvalidConfiguration;
@@ -727,14 +784,38 @@ int implicit_max_ctas_per_sm(const SinkArgs& a) {
     int occ = 0;
     return launch_implicit_warp(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0;
   }
-  const bool fact = a.hrow[0] != nullptr;
+  const int mode = a.stab ? 2 : (a.hrow[0] != nullptr ? 1 : 0);
 #define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
-  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) \
-    return fact ? occupancy_cfg<TS_, TM_, NV_, TR_, D_, true, P_>()                            \
-                : occupancy_cfg<TS_, TM_, NV_, TR_, D_, false, P_>();
+  if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) { \
+    if (mode == 2) {                                                                           \
+      int occ = 0;                                                                             \
+      return stab_cfg<TS_, TM_, NV_, TR_, D_, P_>(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0; \
+    }                                                                                          \
+    return mode == 1 ? occupancy_cfg<TS_, TM_, NV_, TR_, D_, 1, P_>()                          \
+                     : occupancy_cfg<TS_, TM_, NV_, TR_, D_, 0, P_>();                         \
+  }
   LSK_IMPL_ALL(X)
 #undef X
   return 0;
+}
+
+cudaError_t launch_row_shift(const float* X, int64_t n, int d, const float* Wt,
+                             const float* beta2, int r, float c2, float* m2, double* A,
+                             cudaStream_t s) {
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const size_t dyn = sizeof(float) * (d + 1) * r;
+  switch (d) {
+#define C(D_)                                                                                  \
+  case D_:                                                                                     \
+    cudaFuncSetAttribute(impl::row_shift_kernel<D_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn); \
+    impl::row_shift_kernel<D_><<<blocks, 256, dyn, s>>>(X, n, Wt, beta2, r, c2, m2, A);         \
+    break;
+    C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
+#undef C
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_row_scale(const float* X, int64_t n, int d, float c2, float abar, float* h,

@@ -65,8 +65,9 @@ struct SinkArgs {
   float c2;                // -2 log2e / eps
   // implicit factored exponent (FACT): F_jk = h_j * 2^(beta2_k + abar + sum_c W_kc p_jc),
   // h_j = 2^(alpha2_j - abar) precomputed per row; NULL = plain expanded form
-  const float* hrow[2];
+  const float* hrow[2];    // FACT: h_j; stabilised (stab = 1): the per-row shifts m_j
   float abar;
+  int stab;                // 1: stabilised implicit mode (reading C30)
   int dbg;                 // tuning only: 1 = consumers release stages without computing
   unsigned long long* trace;   // tuning only: [pass][cta][4] globaltimer stamps, or NULL
   float l2_resident;       // fraction of each CTA's rows per factor kept L2-resident (evict_last)
@@ -100,6 +101,10 @@ cudaError_t launch_implicit_warp(const SinkArgs& a, bool cooperative, int grid, 
                                  int* occ);
 cudaError_t launch_implicit(const SinkArgs& a, bool cooperative, int grid, cudaStream_t s);
 int implicit_max_ctas_per_sm(const SinkArgs& a);
+// stabilised implicit mode: per-row shifts m_j (fp32) and fp64 log offsets A_j (reading C30)
+cudaError_t launch_row_shift(const float* X, int64_t n, int d, const float* Wt,
+                             const float* beta2, int r, float c2, float* m2, double* A,
+                             cudaStream_t s);
 // h_j = 2^(c2 |p_j|^2 - abar) for the factored exponent (one launch per solve and side)
 cudaError_t launch_row_scale(const float* X, int64_t n, int d, float c2, float abar, float* h,
                              cudaStream_t s);

@@ -11,9 +11,10 @@ X, Y, a, b = (torch.from_numpy(prob[k]).cuda() for k in ("X", "Y", "a", "b"))
 for eps in (0.1, 0.05, 0.02, 0.015, 0.01, 0.007, 0.005):
     ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], eps, cfg.r, cfg.anchor_seed, T=300)
     line = "eps %.3f oracle rot %.8f" % (eps, ref["rot"])
-    try:
-        res = L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=300, stabilize=True)
-        line += " | stab %.8f rel %.1e" % (res["rot"], abs(res["rot"] - ref["rot"]) / abs(ref["rot"]))
-    except Exception as e:
-        line += " | stab FAIL %s" % str(e)[:70]
+    for var in ("stream", "implicit"):
+        try:
+            res = L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=300, stabilize=True, variant=var)
+            line += " | %s-stab %.8f rel %.1e" % (var, res["rot"], abs(res["rot"] - ref["rot"]) / abs(ref["rot"]))
+        except Exception as e:
+            line += " | %s-stab FAIL %s" % (var, str(e)[:40])
     print(line, flush=True)

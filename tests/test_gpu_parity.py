@@ -617,17 +617,19 @@ def test_stabilized_feature_map_matches_oracle(L, eps):
     assert np.max(np.abs(A.cpu().numpy() - Aref) / np.maximum(1.0, np.abs(Aref))) <= 1e-5
 
 
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
 @pytest.mark.parametrize("eps", [0.02, 0.01])
-def test_stabilized_small_eps_rot(L, eps):
-    """At eps where the plain fp32 path breaks down (0.01) or loses digits (0.02), the
-    stabilised stream path matches the fp64 oracle: W_hat within 1e-5 of the plain oracle's
+def test_stabilized_small_eps_rot(L, eps, variant):
+    """At eps where the plain fp32 paths break down (0.01; the implicit one already at 0.02),
+    the stabilised paths (stream: row-normalised stored factors; implicit: per-row exponent
+    shift inside the kernel) match the fp64 oracle: W_hat within 1e-5 of the plain oracle's
     value, and the scalings of the normalised problem within 1e-4 of the oracle run of the same
     formulation (C30: Alg. 1 on the row-normalised factors from u~ = 1)."""
     cfg = synth.get_config(2)
     prob = synth.make_problem(cfg, n=4000, m=3999)
     T = 300
     ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], eps, cfg.r, cfg.anchor_seed, T=T)
-    res = _run_gpu_stab(L, prob, eps, T)
+    res = _run_gpu_stab(L, prob, eps, T, variant)
     assert abs(res["rot"] - ref["rot"]) <= 1e-5 * abs(ref["rot"]), (res["rot"], ref["rot"])
     R = O.max_norm(prob["X"], prob["Y"])
     prm = O.gaussian_params(eps, cfg.d, cfg.r, R)
@@ -638,7 +640,8 @@ def test_stabilized_small_eps_rot(L, eps):
     assert _maxrel(res["u"], s["u"]) <= 1e-4 and _maxrel(res["v"], s["v"]) <= 1e-4
 
 
-def _run_gpu_stab(L, prob, eps, T):
+def _run_gpu_stab(L, prob, eps, T, variant="stream"):
     X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
     cfg = synth.get_config(2)
-    return L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, stabilize=True)
+    return L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, stabilize=True,
+                 variant=variant)
