@@ -98,8 +98,9 @@ __global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
     const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int mode,
     int sdeg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array itself: an integer round
+  // trip would drop the address space and turn every smem access below into a generic LD/ST
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* beta_s = reinterpret_cast<float*>(smem + kOffBeta);
   float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -210,39 +211,48 @@ __global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
   const int row = q4 * 32 + lane;
   const int64_t orow = m0 + row;
   const float al = alpha_s[row];
+  // two 32-column TMEM loads in flight per wait (the epilogue was TMEM-latency bound)
 #pragma unroll 1
-  for (int cc = 0; cc < 4; ++cc) {
-    const int col = half * 128 + cc * 32;
-    uint32_t a[32];
-    const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)col;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
-          "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]),
-          "=r"(a[13]), "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]),
-          "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]),
-          "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]),
-          "=r"(a[31])
-        : "r"(taddr));
+  for (int cp = 0; cp < 4; cp += 2) {
+    uint32_t a[2][32];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int col = half * 128 + (cp + h2) * 32;
+      const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)col;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(a[h2][0]), "=r"(a[h2][1]), "=r"(a[h2][2]), "=r"(a[h2][3]), "=r"(a[h2][4]),
+            "=r"(a[h2][5]), "=r"(a[h2][6]), "=r"(a[h2][7]), "=r"(a[h2][8]), "=r"(a[h2][9]),
+            "=r"(a[h2][10]), "=r"(a[h2][11]), "=r"(a[h2][12]), "=r"(a[h2][13]), "=r"(a[h2][14]),
+            "=r"(a[h2][15]), "=r"(a[h2][16]), "=r"(a[h2][17]), "=r"(a[h2][18]), "=r"(a[h2][19]),
+            "=r"(a[h2][20]), "=r"(a[h2][21]), "=r"(a[h2][22]), "=r"(a[h2][23]), "=r"(a[h2][24]),
+            "=r"(a[h2][25]), "=r"(a[h2][26]), "=r"(a[h2][27]), "=r"(a[h2][28]), "=r"(a[h2][29]),
+            "=r"(a[h2][30]), "=r"(a[h2][31])
+          : "r"(taddr));
+    }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (orow < M) {
-      float* dst = Xi + orow * ld + n0 + col;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        if (n0 + col + j < r) {
-          float o[4];
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int col = half * 128 + (cp + h2) * 32;
+        float* dst = Xi + orow * ld + n0 + col;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float acc = __uint_as_float(a[j + e]);
-            if (mode == 0) {
-              o[e] = ex2(al + beta_s[col + j + e] + acc);
-            } else {
-              const float rl = fmaxf(acc, 0.f);
-              o[e] = beta_s[col + j + e] * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
+        for (int j = 0; j < 32; j += 4) {
+          if (n0 + col + j < r) {
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float acc = __uint_as_float(a[h2][j + e]);
+              if (mode == 0) {
+                o[e] = ex2(al + beta_s[col + j + e] + acc);
+              } else {
+                const float rl = fmaxf(acc, 0.f);
+                o[e] = beta_s[col + j + e] * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
+              }
             }
+            st_global_cs(reinterpret_cast<float4*>(dst + j), make_float4(o[0], o[1], o[2], o[3]));
           }
-          st_global_cs(reinterpret_cast<float4*>(dst + j), make_float4(o[0], o[1], o[2], o[3]));
         }
       }
     }
