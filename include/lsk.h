@@ -178,6 +178,17 @@ lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float
                                          const float* b, double eps, const lsk_solve_opts* o,
                                          float* u, float* v, lsk_report* reps, void* stream);
 
+/* Batched recompute: `batch` independent problems sharing (p, U), one CTA per problem (the
+ * implicit kernel with no grid barrier), the factors regenerated in every pass.  X (batch, n,
+ * d), Y (batch, m, d), a/u (batch, n), b/v (batch, m); reps: host array of `batch` reports
+ * (nullable).  d <= 8.  Not with LSK_SOLVE_STABILIZE. */
+lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, const float* U,
+                                                  const float* X, int64_t n, const float* Y,
+                                                  int64_t m, int32_t batch, const float* a,
+                                                  const float* b, const lsk_solve_opts* o,
+                                                  float* u, float* v, lsk_report* reps,
+                                                  void* stream);
+
 /* ---- a9: read-out W_hat = eps (a^T log u + b^T log v) in fp64 ------- */
 /* rot_host: host double (the call synchronises).  With comm, partial sums are all-reduced. */
 lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,

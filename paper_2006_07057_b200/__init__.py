@@ -97,6 +97,11 @@ _SIGS = {
                                               c_f32p, c_f32p, ctypes.c_double,
                                               P(lsk_solve_opts), c_f32p, c_f32p,
                                               ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_factored_sinkhorn_implicit_batched": (c_i32, [P(lsk_feature_params), c_f32p, c_f32p,
+                                                       c_i64, c_f32p, c_i64, c_i32, c_f32p,
+                                                       c_f32p, P(lsk_solve_opts), c_f32p,
+                                                       c_f32p, ctypes.c_void_p,
+                                                       ctypes.c_void_p]),
     "lsk_rot_value": (c_i32, [c_f32p, c_f32p, c_f32p, c_f32p, c_i64, c_i64, ctypes.c_double,
                               P(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]),
     "lsk_rot_value_batched": (c_i32, [c_f32p, c_f32p, c_f32p, c_f32p, c_i64, c_i64, c_i32,
@@ -302,6 +307,18 @@ def lsk_factored_sinkhorn_batched(Xi, Zeta, a, b, eps, opts, u, v, report=True, 
                                             _f32(v), reps, _stream(stream))
     _check(st, "lsk_factored_sinkhorn_batched")
     return list(reps) if reps is not None else None
+
+
+def lsk_factored_sinkhorn_implicit_batched(p, U, X, Y, a, b, opts, u, v, report=True,
+                                           stream=None):
+    """X (B, n, d), Y (B, m, d), a/u (B, n), b/v (B, m): B independent recompute solves."""
+    B = X.shape[0]
+    reps = (lsk_report * B)() if report else None
+    _check(_lib.lsk_factored_sinkhorn_implicit_batched(
+        ctypes.byref(p), _f32(U), _f32(X), X.shape[1], _f32(Y), Y.shape[1], B, _f32(a), _f32(b),
+        ctypes.byref(opts), _f32(u), _f32(v), reps, _stream(stream)),
+        "lsk_factored_sinkhorn_implicit_batched")
+    return list(reps) if report else None
 
 
 def lsk_rot_value(u, v, a, b, eps, comm=None, stream=None) -> float:

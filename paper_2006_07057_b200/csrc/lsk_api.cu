@@ -711,6 +711,42 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   return st;
 }
 
+lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, const float* U,
+                                                  const float* X, int64_t n, const float* Y,
+                                                  int64_t m, int32_t batch, const float* a,
+                                                  const float* b, const lsk_solve_opts* o,
+                                                  float* u, float* v, lsk_report* reps,
+                                                  void* stream) {
+  if (!p) return fail(LSK_EINVAL, "params NULL");
+  LSK_TRY(check_common(n, m, p->r, p->eps));
+  if (batch < 1) return fail(LSK_EINVAL, "batch must be >= 1");
+  if (!U || !X || !Y || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  if (o && (o->flags & LSK_SOLVE_STABILIZE))
+    return fail(LSK_EUNSUPPORTED, "the stabilised implicit solve is single-problem");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, batch, 2 * num_sms(), n), &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  SinkArgs A{};
+  A.X[0] = X; A.X[1] = Y;
+  A.rows[0] = n; A.rows[1] = m;
+  A.fstride[0] = n * p->d; A.fstride[1] = m * p->d;   // point rows per problem
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.wstride[0] = n; A.wstride[1] = m;
+  A.r = p->r; A.d = p->d; A.eps = p->eps;
+  A.Wt = Wt; A.beta2 = b2;
+  A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
+  LSK_TRY(setup_fact(A, p->R, batch, s, ws, cv));
+  return run_solve(A, true, batch, o, reps, nullptr, s, ws, cv);
+}
+
 lsk_status lsk_implicit_row_offsets(const lsk_feature_params* p, const float* U, const float* X,
                                     int64_t n, double* logoff, void* stream) {
   if (!p || !U || !X || !logoff) return fail(LSK_EINVAL, "NULL argument");

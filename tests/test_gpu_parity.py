@@ -220,6 +220,32 @@ def test_config4_batched_matches_oracle_and_single(L):
 
 
 # ------------------------------------------------------------------ modes & properties ----
+@pytest.mark.parametrize("cfg_key,B,n,m,r", [(1, 5, 500, 487, 100), (5, 3, 2049, 1999, 512)])
+def test_implicit_batched_matches_oracle_and_single(L, cfg_key, B, n, m, r):
+    """B independent recompute solves in one launch (one CTA per problem): each equals the
+    oracle and the single-problem implicit solve of the same pair."""
+    import torch
+    cfg = synth.get_config(cfg_key)
+    probs = [synth.make_problem(cfg, n=n, m=m) if k == 0 else synth.random_small(k, n, m, cfg.d, 0.3)
+             for k in range(B)]
+    X = _dev(np.stack([q["X"] for q in probs])); Y = _dev(np.stack([q["Y"] for q in probs]))
+    a = _dev(np.stack([q["a"] for q in probs])); b = _dev(np.stack([q["b"] for q in probs]))
+    R = max(O.max_norm(q["X"], q["Y"]) for q in probs)
+    p = L.lsk_feature_params_init(cfg.eps, cfg.d, r, R, cfg.anchor_seed)
+    U = torch.empty((r, cfg.d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    T = 60
+    u = torch.empty((B, n), device="cuda"); v = torch.empty((B, m), device="cuda")
+    reps = L.lsk_factored_sinkhorn_implicit_batched(p, U, X, Y, a, b, L.make_opts(T), u, v)
+    for k in range(B):
+        q = probs[k]
+        ref = O.rot(q["X"], q["Y"], q["a"], q["b"], cfg.eps, r, cfg.anchor_seed, T=T, R=R)
+        _check_parity(dict(rot=reps[k].rot, u=u[k], v=v[k]), ref)
+        u1 = torch.empty(n, device="cuda"); v1 = torch.empty(m, device="cuda")
+        rep1 = L.lsk_factored_sinkhorn_implicit(p, U, X[k], Y[k], a[k], b[k], L.make_opts(T), u1, v1)
+        assert abs(rep1.rot - reps[k].rot) <= 1e-6 * abs(rep1.rot)
+
+
 def test_tolerance_mode(L):
     cfg = synth.get_config(1)
     prob = synth.make_problem(cfg)
