@@ -14,20 +14,24 @@
 // when (log2e/eps) R^2 <= 60 (G, h stay far from the fp32 range limits); otherwise the plain
 // expanded form (h = 1, abar folded per row) runs.
 //
+// Stabilised mode (MODE 2, reading C30): each row's exponent is shifted by its maximum
+// m_j = max_k (beta2_k + W_k . p_j) (precomputed, row_shift_kernel), so every regenerated entry
+// is <= ~1, and the kernel returns the scalings of the row-normalised problem.
+//
 // Layout: one CTA per SM made of TEAMS teams of TS threads (all consumers).  A team owns every
 // column: thread t of a team owns float4 column groups {t, t+TS, ...} (its W, beta2, slice of
 // s and fp32 accumulators live in registers; the fp64 accumulators in shared memory).  Teams
 // take alternate tiles of TR rows of the CTA's row range.  Each team's warp 0 stages tiles
-// (point rows, c_j, h_j, v_old_j) kAhead tiles ahead with cp.async into an 8-slot ring whose
-// completion is tracked on per-slot mbarriers.
+// (point rows, c_j, h_j, v_old_j) kAhead = 8 tiles ahead with cp.async into a 16-slot ring.
 //
-// Software pipeline (per team, lag one tile): tile t's features are generated and its row-dot
-// partials published (red[t%3], split mbarrier arrive) BEFORE tile t-1 is finished (wait,
-// scalings, accumulation), so the cross-warp exchange latency of one tile overlaps the MUFU
-// work of the next.  The exchange is spread over lanes: row i's NWT warp partials are summed
-// by G lanes (NWT/G each) and a fixed xor butterfly — every lane of the group ends with the
-// same bits, and the order never changes (deterministic).  Pass boundary, stopping test and
-// the fp64 read-out are those of the streaming kernel (lsk_sinkhorn.cu).
+// Per tile (default, PIPE = 0): features -> row-dot partials -> warp transpose-reduce -> one
+// named barrier per team (publishes the partials and the next slot) -> the exchange: row i's
+// NWT warp partials are summed by G lanes (NWT/G each) and a fixed xor butterfly — every lane of
+// the group ends with the same bits, and the order never changes (deterministic) -> scalings
+// -> FFMA2 accumulation.  PIPE = 1 (tuning alternative) holds two feature tiles: tile t's
+// partials are published with a split mbarrier arrive before tile t-1 is finished.  Pass
+// boundary, stopping test and the fp64 read-out are those of the streaming kernel
+// (lsk_sinkhorn.cu); s is staged once per CTA into shared memory at each pass start.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
