@@ -17,7 +17,7 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblsk.so")
+LIB_PATH = os.environ.get("LSK_LIB_PATH") or os.path.join(_HERE, "liblsk.so")   # override: tuning builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("liblsk.so not built: run `python -m paper_2006_07057_b200.build` "

@@ -182,6 +182,59 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 
   float* tslots = slots + team * kRing * SLOT;
 
+  // What the loader streams for pass p: this CTA's rows of the pass's factor side (c_j, h_j,
+  // v_old_j, point rows).  Pass p+1's first kAhead tiles are issued at the end of pass p, so
+  // their latency hides behind the pass boundary (the inputs are static; v_old was written by
+  // this CTA two passes earlier).
+  struct Feed {
+    const float *w, *X, *h, *vold;
+    int nrows, ntiles;
+  };
+  int64_t rbeg[2];   // this CTA's rows of each side (pass-invariant)
+  int rcnt[2];
+#pragma unroll
+  for (int fs = 0; fs < 2; ++fs) {
+    int64_t q1;
+    cta_rows(A.rows[fs], A.gpp, cta, &rbeg[fs], &q1);
+    rcnt[fs] = (int)(q1 - rbeg[fs]);
+  }
+  auto make_feed = [&](int q) {
+    const int kq = pass_kind(q, A);
+    const int fq = (kq == PK_V || kq == PK_ERR) ? 1 : 0;
+    const int64_t q0 = rbeg[fq];
+    Feed fd;
+    fd.nrows = rcnt[fq];
+    fd.ntiles = ((fd.nrows + TR - 1) / TR - team + TEAMS - 1) / TEAMS;   // tiles team, team+TEAMS, ...
+    fd.w = A.w[fq] + (int64_t)prob * A.wstride[fq] + q0;
+    fd.X = A.X[fq] + (int64_t)prob * A.fstride[fq] + q0 * D;
+    fd.h = (FACT || STAB) ? A.hrow[fq] + (int64_t)prob * A.wstride[fq] + q0 : nullptr;
+    const bool nv = (kq == PK_ERR) || (kq == PK_V && q >= 3);
+    fd.vold = nv ? vbuf_ptr(A, prob, (kq == PK_ERR) ? A.T : (q + 1) / 2 - 1) + q0 : nullptr;
+    return fd;
+  };
+  // loader (team warp 0): tile t of a pass -> slot (g0 + t) % kRing.  PIPE: completion on the
+  // slot's mbarrier; !PIPE: one cp.async group per tile (empty ones too), waited by the loader
+  // before the team's per-tile named barrier publishes the slot
+  auto issue_tile = [&](const Feed& fd, uint32_t g0, int t) {
+    if (t >= fd.ntiles) {
+      if constexpr (!PIPE) cp_async_commit();
+      return;
+    }
+    const int lr = (team + t * TEAMS) * TR;
+    const uint32_t gi = g0 + (uint32_t)t;
+    float* sl = tslots + (gi % kRing) * SLOT;
+    if (lane < TR && lane < fd.nrows - lr) {
+      cp_async4(sl + lane, fd.w + lr + lane);
+      if (FACT || STAB) cp_async4(sl + 32 + lane, fd.h + lr + lane);
+      if (fd.vold) cp_async4(sl + 64 + lane, fd.vold + lr + lane);
+#pragma unroll
+      for (int c = 0; c < D; ++c) cp_async4(sl + 96 + lane * XS + c, fd.X + (lr + lane) * D + c);
+    }
+    if constexpr (PIPE) cp_async_mbar_arrive_noinc(&S.full[team][gi % kRing]);
+    else cp_async_commit();
+  };
+  bool prefetched = false;   // this pass's first kAhead tiles were issued by the previous pass
+
   for (int p = A.pass_begin;; ++p) {
     // ---------------- results of pass q = p-1: stopping test (see lsk_sinkhorn.cu) -------
     const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
@@ -252,17 +305,11 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc_s[j * 4 + q][tid] = 0.0;
 
-    int64_t r0, r1;
-    cta_rows(A.rows[f], A.gpp, cta, &r0, &r1);
-    const int nrows = (int)(r1 - r0);
-    const int ntiles_cta = (nrows + TR - 1) / TR;
-    const int ntiles = (ntiles_cta - team + TEAMS - 1) / TEAMS;   // this team: tiles team, team+TEAMS, ...
-    const float* wp0 = A.w[f] + (int64_t)prob * A.wstride[f] + r0;
-    const float* Xp0 = A.X[f] + (int64_t)prob * A.fstride[f] + r0 * D;
-    const float* hp0 = (FACT || STAB) ? A.hrow[f] + (int64_t)prob * A.wstride[f] + r0 : nullptr;
-    const bool need_vold = (kind == PK_ERR) || (kind == PK_V && p >= 3);
-    const float* vold0 =
-        need_vold ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) + r0 : nullptr;
+    const int64_t r0 = rbeg[f];
+    const Feed feed = make_feed(p);
+    const int nrows = feed.nrows;
+    const int ntiles = feed.ntiles;
+    const bool need_vold = feed.vold != nullptr;
     float* outp0 = nullptr;
     if (kind == PK_U) outp0 = A.out[0] + (int64_t)prob * A.wstride[0] + r0;
     if (kind == PK_V) outp0 = vbuf_ptr(A, prob, (p + 1) / 2) + r0;
@@ -278,31 +325,12 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       constexpr bool kDot = KIND != PK_INIT;
       constexpr bool kAcc = KIND != PK_ERR;
       constexpr bool kOut = KIND == PK_U || KIND == PK_V;
-      // loader (team warp 0): tile t -> slot (gt0+t) % kRing.  v_old_j was written two passes
-      // earlier by this CTA (same rows, same tiling), so plain cp.async ordering suffices.
-      // PIPE: completion on the slot's mbarrier; !PIPE: one cp.async group per tile (empty ones
-      // too), waited by the loader before the team's per-tile named barrier publishes the slot
-      auto issue = [&](int t) {
-        if (t >= ntiles) {
-          if constexpr (!PIPE) cp_async_commit();
-          return;
-        }
-        const int lr = (team + t * TEAMS) * TR;
-        const uint32_t gi = gt0 + (uint32_t)t;
-        float* sl = tslots + (gi % kRing) * SLOT;
-        if (lane < TR && lane < nrows - lr) {
-          cp_async4(sl + lane, wp0 + lr + lane);
-          if (FACT || STAB) cp_async4(sl + 32 + lane, hp0 + lr + lane);
-          if (need_vold) cp_async4(sl + 64 + lane, vold0 + lr + lane);
-#pragma unroll
-          for (int c = 0; c < D; ++c) cp_async4(sl + 96 + lane * XS + c, Xp0 + (lr + lane) * D + c);
-        }
-        if constexpr (PIPE) cp_async_mbar_arrive_noinc(&S.full[team][gi % kRing]);
-        else cp_async_commit();
-      };
+      auto issue = [&](int t) { issue_tile(feed, gt0, t); };
       if (twarp == 0) {
+        if (!prefetched) {
 #pragma unroll
-        for (int t = 0; t < kAhead; ++t) issue(t);
+          for (int t = 0; t < kAhead; ++t) issue(t);
+        }
         if constexpr (!PIPE) cp_async_wait<kAhead - 1>();   // tile 0 landed
       }
       if constexpr (!PIPE) named_bar(team_bar, TS);
@@ -344,7 +372,11 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
               float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);   // STAB: al2 = -m_j
 #pragma unroll
               for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
+#ifdef LSK_ABL_EX2
+              fr[i][j][h] = e;
+#else
               fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
+#endif
             }
           }
         }
@@ -361,14 +393,20 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
             }
             pr[i] = pp.x + pp.y;
           }
+#ifdef LSK_ABL_XCH
+          const float tot = pr[lane % TR];
+#else
           const float tot = warp_transpose_reduce<TR>(pr, lane);
+#endif
           if ((lane & (LPR - 1)) == 0) S.red[team][rb][lane / LPR][twarp] = tot;
         }
         if constexpr (PIPE) {
           mbar_arrive(&S.redbar[team][rb]);   // also the per-tile team sync of the init pass
         } else {
           if (twarp == 0) cp_async_wait<kAhead - 1>();   // tile t+1 landed
+#ifndef LSK_ABL_BAR
           named_bar(team_bar, TS);   // publishes red[rb] and slot t+1 to the team
+#endif
         }
       };
 
@@ -468,7 +506,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       case PK_U: run_tiles(std::integral_constant<int, PK_U>{}); break;
       default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
     }
-    gt += (uint32_t)((ntiles_cta - team + TEAMS - 1) / TEAMS);
+    gt += (uint32_t)ntiles;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
@@ -551,8 +589,26 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       }
       named_bar(1, NT);
     }
+    // issue the next pass's first tiles now, after this CTA's share of the boundary work, so
+    // they land while the CTA waits for the other CTAs' totals (slots gt.. are free: the ring
+    // holds 2 * kAhead tiles)
+    prefetched = false;
+    if constexpr (!PIPE) {
+      const int q = p + 1;
+      if (q < A.pass_end && pass_kind(q, A) != PK_NONE) {
+        if (twarp == 0) {
+          const Feed nf = make_feed(q);
+#pragma unroll
+          for (int t = 0; t < kAhead; ++t) issue_tile(nf, gt, t);
+        }
+        prefetched = true;
+      }
+    }
   }
 
+  if constexpr (!PIPE) {
+    if (twarp == 0) cp_async_wait<0>();   // a prefetch for a pass that did not run
+  }
   if (final_t >= 0) {
     // returned v into the user buffer, then W_hat = eps (a^T log u + b^T log v) in fp64
     int64_t u0, u1, v0, v1;
@@ -723,7 +779,12 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_ALL(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
   LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                   \
   LSK_IMPL_D123(X, 256, 1, 4, 8, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                  \
-  LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2)
+  LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2) LSK_IMPL_EXTRA(X)
+#ifdef LSK_IMPL_EXTRA_H   // tuning builds add instantiations (scripts/build_variant.sh)
+#include LSK_IMPL_EXTRA_H
+#else
+#define LSK_IMPL_EXTRA(X)
+#endif
 
 template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
