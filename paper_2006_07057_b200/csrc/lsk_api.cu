@@ -336,9 +336,10 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.nstage = c.nstage;
   A.stage_floats = c.stage_floats;
   const int64_t rs = A.r + kExtra;
-  // part: [batch][r + kExtra + 2][gpp] (the last two columns carry the read-out partials);
+  // part: [batch][(r + kExtra + 4) / 4 blocks][gpp][4] (block r/4 + 1 carries the read-out
+  // partials; lsk_sink_common.cuh);
   // svec: [batch][2][r + kExtra], armed with the all-ones sentinel (lsk_sink_common.cuh)
-  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * (rs + 2) * c.gpp * batch));
+  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * (rs + 4) * c.gpp * batch));
   A.svec = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * 2 * rs * batch));
   LSK_CU(cudaMemsetAsync(A.svec, 0xFF, sizeof(double) * 2 * rs * batch, s));
   A.state = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * kStateDoubles * batch));

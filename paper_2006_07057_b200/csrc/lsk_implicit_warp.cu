@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
 
   float4 s[NV];
   const int64_t rstride = r + kExtra;
-  double* part = A.part + (int64_t)prob * (rstride + 2) * A.gpp;   // [r + kExtra + 2][gpp]
+  double* part = A.part + prob * part_per_problem(r, A.gpp);   // [blk][gpp][4]
   const bool multi = A.multi_launch != 0;
   unsigned int nbar = 0;
 
@@ -389,24 +389,13 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
       for (int e = tid; e < NE * 32; e += NT) {   // element e = (4 j + q) * 32 + l: column 4(l + 32 j) + q
         const int l = e & 31, jq = e >> 5;
         const int col = 4 * (l + 32 * (jq >> 2)) + (jq & 3);
-        if (col < r) part[(int64_t)col * A.gpp + cta] = accw[e];
+        if (col < r) *part_at(part, A.gpp, col, cta) = accw[e];
       }
-      if (tid == 0) {
-        part[(int64_t)(r + 0) * A.gpp + cta] = e0;
-        part[(int64_t)(r + 1) * A.gpp + cta] = e1;
-        part[(int64_t)(r + 2) * A.gpp + cta] = 0.0;
-        part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
-      }
+      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, 0.0, 0.0);
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[1] = globaltimer();
-      for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NWARP) {
-        const double* col = part + (int64_t)k * A.gpp;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
-        acc = warp_sum_f64(acc);
-        if (lane == 0) sv_publish(A, prob, p, k, acc);
-      }
+      // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
+      for (int kb = cta + A.gpp * warp; kb <= (r >> 2); kb += A.gpp * NWARP) r2_block(A, prob, p, part, kb, lane);
       if (trc) trc[2] = globaltimer();
       if (trc) trc[3] = globaltimer();
     } else {
@@ -452,16 +441,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
     }
     if (A.gpp > 1) {
       if (tid == 0) {
-        part[(int64_t)rstride * A.gpp + cta] = la;        // columns r+kExtra, r+kExtra+1:
-        part[(int64_t)(rstride + 1) * A.gpp + cta] = lb;  // never read by R2 (no race with it)
+        *part_at(part, A.gpp, (int)rstride, cta) = la;       // columns r+kExtra, r+kExtra+1:
+        *part_at(part, A.gpp, (int)rstride + 1, cta) = lb;   // never read by R2 (no race with it)
       }
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (cta == 0 && tid == 0) {
         la = 0.0;
         lb = 0.0;
         for (int c = 0; c < A.gpp; ++c) {
-          la += __ldcg(part + (int64_t)rstride * A.gpp + c);
-          lb += __ldcg(part + (int64_t)(rstride + 1) * A.gpp + c);
+          la += __ldcg(part_at(part, A.gpp, (int)rstride, c));
+          lb += __ldcg(part_at(part, A.gpp, (int)rstride + 1, c));
         }
       }
     }

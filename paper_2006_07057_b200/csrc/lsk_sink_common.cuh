@@ -152,6 +152,58 @@ __device__ __forceinline__ void sv_publish(const SinkArgs& A, int prob, int pass
   }
 }
 
+// ---- R1/R2 partial layout: column blocks of 4, part[blk][cta][4] ---------------------------
+// Per problem (r + kExtra + 4) * gpp doubles: blocks 0..r/4-1 the r-vector, block r/4 the
+// extras (err, breakdowns, 0, 0), block r/4+1 the read-out partials.  A CTA's four partials
+// of a block are one 32-byte sector (R1: one coalesced store pair per float4 group instead of
+// four scattered 8-byte stores, so the barrier's release drains fewer stores), and a block's
+// partials of all CTAs are contiguous (R2 reads 32 * gpp consecutive bytes).
+__device__ __forceinline__ int64_t part_per_problem(int r, int gpp) {
+  return (int64_t)(r + kExtra + 4) * gpp;
+}
+__device__ __forceinline__ double* part_at(double* part, int gpp, int k, int cta) {
+  return part + (((int64_t)(k >> 2) * gpp + cta) << 2) + (k & 3);
+}
+__device__ __forceinline__ void part_store4(double* part, int gpp, int blk, int cta, double a0,
+                                            double a1, double a2, double a3) {
+  double2* d = reinterpret_cast<double2*>(part + (((int64_t)blk * gpp + cta) << 2));
+  d[0] = make_double2(a0, a1);
+  d[1] = make_double2(a2, a3);
+}
+
+// R2 of column block kb (columns 4kb..4kb+3) by one warp: every lane adds the partials of the
+// CTAs it reads in increasing CTA order (double2 e = lane + 32 i holds CTA e/2's columns
+// 2(e&1), 2(e&1)+1), then an xor butterfly over the lanes of equal parity — a fixed order, the
+// same bits on every run — and lanes 0, 1 publish the four totals.
+__device__ __forceinline__ void sv_publish(const SinkArgs& A, int prob, int pass, int k, double v);
+__device__ __forceinline__ void r2_block(const SinkArgs& A, int prob, int pass, const double* part,
+                                         int kb, int lane) {
+  const double2* src = reinterpret_cast<const double2*>(part + (((int64_t)kb * A.gpp) << 2));
+  const int n2 = 2 * A.gpp;
+  double ax = 0.0, ay = 0.0;
+  constexpr int kBatch = 10;   // loads in flight per lane (one L2 round trip for gpp <= 160)
+  for (int e0 = lane; e0 < n2; e0 += 32 * kBatch) {
+    double2 v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i)
+      v[i] = (e0 + 32 * i < n2) ? __ldcg(src + e0 + 32 * i) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      ax += v[i].x;
+      ay += v[i].y;
+    }
+  }
+#pragma unroll
+  for (int off = 2; off <= 16; off <<= 1) {
+    ax += __shfl_xor_sync(0xffffffffu, ax, off);
+    ay += __shfl_xor_sync(0xffffffffu, ay, off);
+  }
+  if (lane < 2) {
+    sv_publish(A, prob, pass, 4 * kb + 2 * lane, ax);
+    sv_publish(A, prob, pass, 4 * kb + 2 * lane + 1, ay);
+  }
+}
+
 __device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
   return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];
 }

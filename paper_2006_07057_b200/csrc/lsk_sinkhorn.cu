@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   // running solve state (identical in every CTA of the problem)
   double stErr = __ldcg(stg_state + ST_ERR);
   double stBrk = __ldcg(stg_state + ST_BRK);
-  double* part = A.part + (int64_t)prob * (rstride + 2) * A.gpp;   // [r + kExtra + 2][gpp]
+  double* part = A.part + prob * part_per_problem(r, A.gpp);   // [blk][gpp][4]
   unsigned int nbar = 0;   // group barriers passed for this problem in this launch
   int final_t = -1, conv = 0;
   double ferr = -1.0;
@@ -408,31 +408,17 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
     if (trc) trc[0] = globaltimer();   // tiles done
     if (A.gpp > 1) {
-      // R1: column-major partials part[k * gpp + cta]
+      // R1: block partials part[blk][cta][4] (lsk_sink_common.cuh)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
-        if (gv[j]) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) part[(int64_t)(4 * g[j] + q) * A.gpp + cta] = acc64[j][q];
-        }
+        if (gv[j]) part_store4(part, A.gpp, g[j], cta, acc64[j][0], acc64[j][1], acc64[j][2], acc64[j][3]);
       }
-      if (tid == 0) {
-        part[(int64_t)(r + 0) * A.gpp + cta] = e0;
-        part[(int64_t)(r + 1) * A.gpp + cta] = e1;
-        part[(int64_t)(r + 2) * A.gpp + cta] = 0.0;
-        part[(int64_t)(r + 3) * A.gpp + cta] = 0.0;
-      }
+      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, 0.0, 0.0);
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[1] = globaltimer();   // barrier 1 passed
       // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
-      for (int k = cta + A.gpp * warp; k < r + kExtra; k += A.gpp * NW) {
-        const double* col = part + (int64_t)k * A.gpp;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int i = lane; i < A.gpp; i += 32) acc += __ldcg(col + i);
-        acc = warp_sum_f64(acc);
-        if (lane == 0) sv_publish(A, prob, p, k, acc);
-      }
+      // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
+      for (int kb = cta + A.gpp * warp; kb <= (r >> 2); kb += A.gpp * NW) r2_block(A, prob, p, part, kb, lane);
       if (trc) trc[2] = globaltimer();   // R2 done
       if (trc) trc[3] = globaltimer();   // barrier 2 passed
     } else {
@@ -479,16 +465,16 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     }
     if (A.gpp > 1) {
       if (tid == 0) {
-        part[(int64_t)rstride * A.gpp + cta] = la;        // columns r+kExtra, r+kExtra+1:
-        part[(int64_t)(rstride + 1) * A.gpp + cta] = lb;  // never read by R2 (no race with it)
+        *part_at(part, A.gpp, (int)rstride, cta) = la;       // columns r+kExtra, r+kExtra+1:
+        *part_at(part, A.gpp, (int)rstride + 1, cta) = lb;   // never read by R2 (no race with it)
       }
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (cta == 0 && tid == 0) {
         la = 0.0;
         lb = 0.0;
         for (int c = 0; c < A.gpp; ++c) {
-          la += __ldcg(part + (int64_t)rstride * A.gpp + c);
-          lb += __ldcg(part + (int64_t)(rstride + 1) * A.gpp + c);
+          la += __ldcg(part_at(part, A.gpp, (int)rstride, c));
+          lb += __ldcg(part_at(part, A.gpp, (int)rstride + 1, c));
         }
       }
     }
