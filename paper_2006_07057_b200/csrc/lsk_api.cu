@@ -268,19 +268,23 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   const int sms = num_sms();
   if (batch > 1) {
     // persistent groups of gpp CTAs, each looping over problems; pick the group size that
-    // keeps the most SMs busy over all rounds, charging gpp > 1 for its per-pass global
-    // exchange (measured, config 4: 256 problems -> gpp 1 at 1274 it/s beats gpp 4 at 1172
-    // despite 86.5% vs 98.8% balance; small batches spread each problem over many SMs)
+    // keeps the most SMs busy over all rounds, charging gpp > 1 its per-pass group exchange:
+    // t_x ~ 6.4 us against the pass's streaming time at the slot's share of HBM (measured,
+    // config 4, 256 problems: gpp 1 / 2 / 4 / 8 -> 1282 / 1212 / 1312 / 1106 it/s; balance
+    // 86.5% / 86.5% / 98.8% / 92.2%)
     const int slots = sms * cps;
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
+    const double slot_bw = 6.4e12 / slots;   // bytes/s per CTA slot when all stream
     int best_g = 1;
     double best_eff = -1.0;
     for (int gsz = 1; gsz <= 64 && gsz <= slots; gsz *= 2) {
       if (gsz > 1 && rows / gsz < 2 * tr) break;
       const int ngroups = slots / gsz;
       const int rounds = (batch + ngroups - 1) / ngroups;
+      const double t_pass = 4.0 * A.r * (double)rows / gsz / slot_bw;
       const double eff = (double)batch * gsz / ((double)rounds * ngroups * gsz) *
-                         ((double)ngroups * gsz / slots) * (gsz == 1 ? 1.0 : 0.8);
+                         ((double)ngroups * gsz / slots) *
+                         (gsz == 1 ? 1.0 : t_pass / (t_pass + 6.4e-6));
       if (eff > best_eff + 1e-9) { best_eff = eff; best_g = gsz; }
     }
     if (const char* e = getenv("LSK_BGPP")) best_g = std::max(1, atoi(e));   // tuning knob

@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[1] = globaltimer();
       // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
-      for (int kb = cta + A.gpp * warp; kb <= (r >> 2); kb += A.gpp * NW) r2_block(A, prob, p, part, kb, lane);
+      r2_cta(A, prob, p, part, cta, warp, NW, lane);
       if (trc) trc[2] = globaltimer();
       if (trc) trc[3] = globaltimer();
     } else {

@@ -171,36 +171,58 @@ __device__ __forceinline__ void part_store4(double* part, int gpp, int blk, int 
   d[1] = make_double2(a2, a3);
 }
 
-// R2 of column block kb (columns 4kb..4kb+3) by one warp: every lane adds the partials of the
-// CTAs it reads in increasing CTA order (double2 e = lane + 32 i holds CTA e/2's columns
-// 2(e&1), 2(e&1)+1), then an xor butterfly over the lanes of equal parity — a fixed order, the
-// same bits on every run — and lanes 0, 1 publish the four totals.
+// R2 of column block kb (columns 4kb..4kb+3) by G2 lanes of a warp: every lane adds the
+// partials of the CTAs it reads in increasing CTA order (double2 e = sub + G2 i holds CTA e/2's
+// columns 2(e&1), 2(e&1)+1), then an xor butterfly over the group's lanes of equal parity — a
+// fixed order, the same bits on every run — and the group's lanes 0, 1 publish the four totals.
+// G2 = 2 gpp rounded up to a power of two (<= 32): small groups reduce 32 / G2 blocks per warp
+// in one round trip.
 __device__ __forceinline__ void sv_publish(const SinkArgs& A, int prob, int pass, int k, double v);
+__device__ __forceinline__ int r2_lanes(int gpp) {
+  int g = 2;
+  while (g < 2 * gpp && g < 32) g <<= 1;
+  return g;
+}
 __device__ __forceinline__ void r2_block(const SinkArgs& A, int prob, int pass, const double* part,
-                                         int kb, int lane) {
+                                         int kb, int sub, int G2, bool active) {
   const double2* src = reinterpret_cast<const double2*>(part + (((int64_t)kb * A.gpp) << 2));
   const int n2 = 2 * A.gpp;
   double ax = 0.0, ay = 0.0;
   constexpr int kBatch = 10;   // loads in flight per lane (one L2 round trip for gpp <= 160)
-  for (int e0 = lane; e0 < n2; e0 += 32 * kBatch) {
-    double2 v[kBatch];
+  if (active) {
+    for (int e0 = sub; e0 < n2; e0 += G2 * kBatch) {
+      double2 v[kBatch];
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i)
-      v[i] = (e0 + 32 * i < n2) ? __ldcg(src + e0 + 32 * i) : make_double2(0.0, 0.0);
+      for (int i = 0; i < kBatch; ++i)
+        v[i] = (e0 + G2 * i < n2) ? __ldcg(src + e0 + G2 * i) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int i = 0; i < kBatch; ++i) {
-      ax += v[i].x;
-      ay += v[i].y;
+      for (int i = 0; i < kBatch; ++i) {
+        ax += v[i].x;
+        ay += v[i].y;
+      }
     }
   }
-#pragma unroll
-  for (int off = 2; off <= 16; off <<= 1) {
+  for (int off = 2; off < G2; off <<= 1) {
     ax += __shfl_xor_sync(0xffffffffu, ax, off);
     ay += __shfl_xor_sync(0xffffffffu, ay, off);
   }
-  if (lane < 2) {
-    sv_publish(A, prob, pass, 4 * kb + 2 * lane, ax);
-    sv_publish(A, prob, pass, 4 * kb + 2 * lane + 1, ay);
+  if (active && sub < 2) {
+    sv_publish(A, prob, pass, 4 * kb + 2 * sub, ax);
+    sv_publish(A, prob, pass, 4 * kb + 2 * sub + 1, ay);
+  }
+}
+
+// R2 of every column block this CTA owns (kb = cta, cta + gpp, ...; block r/4: the extras),
+// spread over the CTA's nw warps, 32 / G2 blocks per warp at a time
+__device__ __forceinline__ void r2_cta(const SinkArgs& A, int prob, int pass, const double* part,
+                                       int cta, int warp, int nw, int lane) {
+  const int G2 = r2_lanes(A.gpp);
+  const int bpw = 32 / G2;
+  const int nblk = (A.r >> 2) + 1;
+  const int mine = (nblk - cta + A.gpp - 1) / A.gpp;   // blocks owned by this CTA
+  for (int m0 = warp * bpw; m0 < mine; m0 += nw * bpw) {
+    const int m = m0 + lane / G2;
+    r2_block(A, prob, pass, part, cta + A.gpp * m, lane % G2, G2, m < mine);
   }
 }
 

@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (trc) trc[1] = globaltimer();   // barrier 1 passed
       // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
       // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
-      for (int kb = cta + A.gpp * warp; kb <= (r >> 2); kb += A.gpp * NW) r2_block(A, prob, p, part, kb, lane);
+      r2_cta(A, prob, p, part, cta, warp, NW, lane);
       if (trc) trc[2] = globaltimer();   // R2 done
       if (trc) trc[3] = globaltimer();   // barrier 2 passed
     } else {
