@@ -1185,23 +1185,48 @@ lsk_status lsk_comm_enable_p2p(lsk_comm* c, int32_t r_max, void* stream) {
     cudaFree(mine);
     return st;
   }
-  for (int i = 0; i < N; ++i) {
+  cudaError_t open_err = cudaSuccess;
+  for (int i = 0; i < N && open_err == cudaSuccess; ++i) {
     if (i == c->rank) {
       c->xbox[i] = mine;
       continue;
     }
     void* ptr = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&ptr, all[i], cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      for (int j = 0; j < i; ++j)
-        if (j != c->rank && c->xbox[j]) cudaIpcCloseMemHandle(c->xbox[j]);
-      cudaFree(mine);
-      for (auto& x : c->xbox) x = nullptr;
-      return fail(LSK_EUNSUPPORTED, std::string("peer memory unavailable: ") + cudaGetErrorString(e));
-    }
-    c->xbox[i] = static_cast<double*>(ptr);
+    open_err = cudaIpcOpenMemHandle(&ptr, all[i], cudaIpcMemLazyEnablePeerAccess);
+    if (open_err == cudaSuccess) c->xbox[i] = static_cast<double*>(ptr);
+    else cudaGetLastError();
   }
+  // every rank must take the same path (a rank on the in-kernel exchange would wait for peers
+  // on the NCCL path until the timeout): all-gather the local outcome and agree
+  int32_t* flags = nullptr;
+  LSK_CU(cudaMalloc(&flags, sizeof(int32_t) * (N + 1)));
+  const int32_t ok = open_err == cudaSuccess ? 1 : 0;
+  std::vector<int32_t> okv(N, 0);
+  LSK_CU(cudaMemcpyAsync(flags + N, &ok, sizeof(ok), cudaMemcpyHostToDevice, s));
+  st = nccl_check(nccl().allGather(flags + N, flags, 1, ncclInt32, c->comm, s), "ncclAllGather(p2p flags)");
+  if (st == LSK_OK) {
+    LSK_CU(cudaMemcpyAsync(okv.data(), flags, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, s));
+    LSK_CU(cudaStreamSynchronize(s));
+  }
+  bool all_ok = st == LSK_OK;
+  for (int i = 0; i < N; ++i) all_ok = all_ok && okv[i] == 1;
+  if (!all_ok) {
+    for (int j = 0; j < N; ++j)
+      if (j != c->rank && c->xbox[j]) cudaIpcCloseMemHandle(c->xbox[j]);
+    // every rank has closed its mappings before any exporter frees its inbox
+    if (st == LSK_OK) {
+      st = nccl_check(nccl().allGather(flags + N, flags, 1, ncclInt32, c->comm, s), "ncclAllGather(p2p close)");
+      cudaStreamSynchronize(s);
+    }
+    cudaFree(flags);
+    cudaFree(mine);
+    for (auto& x : c->xbox) x = nullptr;
+    if (st != LSK_OK) return st;
+    return fail(LSK_EUNSUPPORTED, open_err != cudaSuccess
+                                      ? std::string("peer memory unavailable: ") + cudaGetErrorString(open_err)
+                                      : std::string("peer memory unavailable on another rank"));
+  }
+  cudaFree(flags);
   c->xrs = xrs;
   c->p2p = true;
   return LSK_OK;
