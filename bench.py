@@ -136,15 +136,17 @@ def run_reference(args):
         t_feat, t_it = t1 - t0, (t2 - t1) / k_iter
         t_feat_all.append(t_feat)
         t_iter_all.append(t_it)
-        step_vals.append(cfg.T / (t_feat + cfg.T * t_it))
+        step_vals.append(cfg.T / (cfg.batch * (t_feat + cfg.T * t_it)))   # B pairs per iteration
     cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] or [os.cpu_count()])
     value = float(np.median(step_vals))
     sample = ("config %d full size (n=m=%d, r=%d): fp64 features + %d of T=%d iterations per "
               "step, extrapolated to T" % (cfg.key, cfg.n, cfg.r, k_iter, cfg.T))
+    if cfg.batch > 1:
+        sample += "; one of the %d pairs, x%d" % (cfg.batch, cfg.batch)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.median([tf + cfg.T * ti for tf, ti in zip(t_feat_all, t_iter_all)])),
+        "ms_per_step": 1e3 * cfg.batch * float(np.median([tf + cfg.T * ti for tf, ti in zip(t_feat_all, t_iter_all)])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": "config%d-%s" % (cfg.key, cfg.name), "n": cfg.n, "m": cfg.m,
@@ -174,11 +176,12 @@ def cpu_baseline(cfg, iters=3):
     O.sinkhorn_factored(xi, zeta, prob["a"], prob["b"], T=iters)
     t2 = time.perf_counter()
     t_it = (t2 - t1) / iters
-    value = cfg.T / ((t1 - t0) + cfg.T * t_it)
+    value = cfg.T / (cfg.batch * ((t1 - t0) + cfg.T * t_it))
     cores = max([int(i.get("num_threads", 0)) for i in threadpool_info()] or [os.cpu_count()])
+    pairs = (" one of the %d pairs, x%d" % (cfg.batch, cfg.batch)) if cfg.batch > 1 else ""
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "config %d full size: fp64 features + %d of T=%d iterations, extrapolated "
-                      "to T (features %.2f s, %.3f s/iteration)" % (cfg.key, iters, cfg.T,
+            "sample": "config %d full size%s: fp64 features + %d of T=%d iterations, extrapolated "
+                      "to T (features %.2f s, %.3f s/iteration)" % (cfg.key, pairs, iters, cfg.T,
                                                                     t1 - t0, t_it)}
 
 
@@ -208,6 +211,8 @@ def run_lsk(args):
     if ws == 1:
         exchange = "none"
     cfg = synth.get_config(args.config)
+    if cfg.batch > 1:
+        return run_lsk_batched(args, cfg, L, torch, dist, comm, ws, rank, local)
     variant = args.variant
     if variant == "auto":
         # measured: the MUFU-recompute variant is faster where it applies
@@ -383,6 +388,119 @@ def run_lsk(args):
     else:
         result["e2e"] = None
 
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cfg, iters=args.ref_iters)
+    if comm is not None:
+        L.lsk_comm_destroy(comm)
+    if dist is not None:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+    return 0
+
+
+def run_lsk_batched(args, cfg, L, torch, dist, comm, ws, rank, local):
+    """Config 4: B independent pairs in one batched solve per step (shared anchor draw, R over
+    all pairs; tcgen05 feature maps; one persistent batched Sinkhorn launch; batched read-out).
+    An iteration is one Sinkhorn iteration of every pair; weak scaling = B pairs per GPU, no
+    cross-GPU exchange (the pairs are independent)."""
+    B, n, m, r, d, T, eps = cfg.batch, cfg.n, cfg.m, cfg.r, cfg.d, cfg.T, cfg.eps
+    dev = torch.device("cuda", local)
+    bp = synth.make_batched(cfg)   # the same B pairs on every rank (independent problems)
+    Xh = torch.from_numpy(bp["X"]).pin_memory()
+    Yh = torch.from_numpy(bp["Y"]).pin_memory()
+    ah = torch.from_numpy(bp["a"]).pin_memory()
+    bh = torch.from_numpy(bp["b"]).pin_memory()
+    X, Y, a, b = (t.to(dev) for t in (Xh, Yh, ah, bh))
+    U = torch.empty((r, d), dtype=torch.float32, device=dev)
+    Xi = torch.empty((B, n, r), dtype=torch.float32, device=dev)
+    Ze = torch.empty((B, m, r), dtype=torch.float32, device=dev)
+    u = torch.empty((B, n), dtype=torch.float32, device=dev)
+    v = torch.empty((B, m), dtype=torch.float32, device=dev)
+    opts = L.make_opts(T, 0.0, False, args.ctas_per_sm)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    peaks, src = _peaks()
+
+    def step(Xs, Ys, As, Bs, ev_k0=None, ev_k1=None):
+        p = L.lsk_feature_params_init(eps, d, r, 0.0, cfg.anchor_seed, Xs.reshape(-1, d), Ys.reshape(-1, d))
+        L.lsk_draw_anchors(p, U)
+        L.lsk_feature_map_batched(p, U, Xs, Xi)
+        L.lsk_feature_map_batched(p, U, Ys, Ze)
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        L.lsk_factored_sinkhorn_batched(Xi, Ze, As, Bs, eps, opts, u, v, report=False)
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+        return L.lsk_rot_value_batched(u, v, As, Bs, eps)
+
+    for _ in range(args.warmup):
+        step(X, Y, a, b)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    L.launch_count(reset=True)
+    step_ms, kern_ms, rots = [], [], None
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rots = step(X, Y, a, b, k0, k1)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kern_ms.append(k0.elapsed_time(k1))
+    launches = L.launch_count()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    tot_ms, kmean = float(np.sum(step_ms)), float(np.mean(kern_ms))
+    if dist is not None:
+        t = torch.tensor([tot_ms, kmean], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, kmean = float(t[0]), float(t[1])
+    value = ws * T * args.steps / (tot_ms / 1e3)
+    rows = n + T * (n + m)
+    alg_bytes = B * (4.0 * r * rows + 8.0 * rows + 4.0 * m * (T - 1))
+    achieved = alg_bytes / (kmean / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % src,
+            "algorithmic_bytes_per_launch": alg_bytes}
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "config%d-%s" % (cfg.key, cfg.name), "variant": "stream-batched",
+                   "batch_per_gpu": B, "n": n, "m": m, "d": d, "r": r, "eps": eps, "T": T,
+                   "iteration": "one Sinkhorn iteration of every pair",
+                   "pair_iterations_per_s": value * B,
+                   "parallelism": "pairs%d" % ws if ws > 1 else "single",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "roofline": roof, "kernel_ms": kmean, "gpu_launches": int(launches), "clocks": clk,
+        "rot_pair0": rots[0] if rots else None,
+    }
+    if ws == 1 and not args.no_e2e:   # host buffers in, ROT values out, copies timed
+        ts = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            Xs, Ys, As, Bs = (t.to(dev, non_blocking=True) for t in (Xh, Yh, ah, bh))
+            step(Xs, Ys, As, Bs)   # rot values come back to the host
+            ts.append(time.perf_counter() - t0)
+        result["e2e"] = {"value": T * len(ts) / float(np.sum(ts)), "unit": UNIT,
+                         "h2d_bytes_per_step": 4 * B * (n * d + m * d + n + m),
+                         "d2h_bytes_per_step": 8 * B}
+    else:
+        result["e2e"] = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cfg, iters=args.ref_iters)
     if comm is not None:
