@@ -425,8 +425,10 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   return LSK_OK;
 }
 
+constexpr double kHybridDefault = 0.0;   // set from the measured sweep (DESIGN.md §6 K5)
+
 static size_t solve_ws_bytes(int r, int64_t m, int batch, int gpp_max, int64_t n = 0) {
-  const int64_t rs = r + kExtra;
+  const int64_t rs = r + kExtra + 4;   // partials: r + kExtra + 4 per CTA (column blocks)
   return 256 * 8 + sizeof(float) * (n + m + 64) * batch +   // implicit row factors h (FACT)
           sizeof(double) * rs * gpp_max * batch + sizeof(double) * rs * batch +
          sizeof(double) * kStateDoubles * batch + sizeof(unsigned) * batch +
@@ -659,6 +661,27 @@ lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, 
   return run_solve(A, false, 1, o, rep, comm, s, ws, cv);
 }
 
+// Fraction of each side's rows the hybrid implicit kernel streams (materialised) instead of
+// regenerating: LSK_HYB=<phi> (0 = off), else the default below for the shapes the hybrid
+// kernel covers (r <= 1024, d <= 3, one CTA-wide team), bounded by a memory budget.
+static double hybrid_fraction(int r, int d, int64_t n, int64_t m) {
+  double phi = kHybridDefault;
+  if (const char* e = getenv("LSK_HYB")) phi = atof(e);
+  if (!(phi > 0.0) || r > 1024 || d > 3) return 0.0;
+  phi = std::min(phi, 0.9);
+  // rows per CTA must leave the recompute team whole tiles to work on
+  if ((double)std::min(n, m) * (1.0 - phi) < 16.0 * num_sms()) return 0.0;
+  // at most a quarter of the device memory (queried once: cudaMemGetInfo costs host ms)
+  static size_t total = 0;
+  if (total == 0) {
+    size_t fr = 0;
+    if (cudaMemGetInfo(&fr, &total) != cudaSuccess) total = 1;
+  }
+  const double bytes = phi * (double)(n + m) * r * 4.0;
+  if (bytes > 0.25 * (double)total) return 0.0;
+  return phi;
+}
+
 lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const float* U,
                                           const float* X, int64_t n, const float* Y, int64_t m,
                                           const float* a, const float* b,
@@ -678,10 +701,18 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   const size_t oM = stab ? cv.take(sizeof(float) * (n + m)) : 0;    // row shifts m_j
   const size_t oA = stab ? cv.take(sizeof(double) * (n + m)) : 0;   // row offsets A_j
   const size_t oR = stab ? cv.take(16384) : 0;                      // read-out scratch
+  // hybrid: the first phi n (phi m) rows are materialised and streamed by extra warps of the
+  // same persistent launch, the rest regenerated (HBM and MUFU busy at once)
+  const double phi = stab ? 0.0 : hybrid_fraction(p->r, p->d, n, m);
+  const int64_t ns0 = (int64_t)(phi * (double)n), ns1 = (int64_t)(phi * (double)m);
+  const bool hyb = ns0 + ns1 > 0;
+  const size_t oD = hyb ? cv.take(sizeof(float) * p->r) : 0;
+  const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r) : 0;
   LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms(), n), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
-  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  float* bD = hyb ? reinterpret_cast<float*>(ws + oD) : nullptr;
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, bD, s));
   SinkArgs A{};
   A.X[0] = X; A.X[1] = Y;
   A.rows[0] = n; A.rows[1] = m;
@@ -701,6 +732,16 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
     A.stab = 1;
   } else {
     LSK_TRY(setup_fact(A, p->R, 1, s, ws, cv));
+  }
+  if (hyb) {
+    float* F0 = reinterpret_cast<float*>(ws + oF);
+    float* F1 = F0 + ns0 * p->r;
+    if (ns0 > 0) LSK_CU(launch_feature_map(X, ns0, p->d, U, Wt, b2, bD, p->r, p->eps, F0, s));
+    if (ns1 > 0) LSK_CU(launch_feature_map(Y, ns1, p->d, U, Wt, b2, bD, p->r, p->eps, F1, s));
+    A.F[0] = F0;
+    A.F[1] = F1;
+    A.nstream[0] = ns0;
+    A.nstream[1] = ns1;
   }
   lsk_status st = run_solve(A, true, 1, o, rep, comm, s, ws, cv);
   if (stab && rep && st >= 0) {

@@ -47,6 +47,8 @@ namespace lsk {
 namespace impl {
 
 constexpr int kRing = 16;   // tile slots per team
+constexpr int kSRing = 6;   // hybrid: row slots per stream warp (bulk copies in flight)
+constexpr int kSRow = 1024; // hybrid: floats per row slot (r <= 1024)
 constexpr int kAhead = 8;   // the loader stages tile t+kAhead when tile t starts (<= kRing/2)
 
 template <int D>
@@ -63,12 +65,14 @@ __host__ __device__ constexpr int exchange_lanes(int nwt, int lpr) {
   return g;
 }
 
-template <int TS, int TEAMS, int TR>
+template <int TS, int TEAMS, int TR, int NWALL, int SW>
 struct Smem {
   uint64_t full[TEAMS][kRing];     // slot landed (32 cp.async arrivals of the loader warp)
   uint64_t redbar[TEAMS][3];       // row-dot partials of a tile published (TS arrivals)
   float red[TEAMS][3][TR][TS / 32];
-  double xs[2][TS * TEAMS / 32];
+  double xs[2][NWALL];
+  double xsS[2][SW > 0 ? SW : 1];  // stream warps' error / breakdown sums of a pass
+  uint64_t sfull[SW > 0 ? SW : 1][kSRing];   // stream warps' row slots landed (bulk copy tx)
   double ext[kExtra];
   double errL[TEAMS][32];          // per-lane marginal-error sums of the output warps
   double brkL[TEAMS][32];          // per-lane breakdown counts of the output warps
@@ -78,12 +82,17 @@ struct Smem {
 
 // MODE 0: expanded exponent; 1: factored (row factor h_j); 2: stabilised (per-row shift m_j,
 // scalings of the row-normalised problem, reading C30)
-template <int TS, int TEAMS, int NV, int TR, int D, int MODE, bool PIPE>
-__global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs A) {
+// SW > 0 (hybrid): SW more warps stream the materialised factor rows [0, nstream) of each side
+// (read once per pass from HBM, which the recompute teams leave idle) while the teams
+// regenerate the rest; both add into the same fixed-order reductions.
+template <int TS, int TEAMS, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
+__global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const SinkArgs A) {
   constexpr bool FACT = MODE == 1, STAB = MODE == 2;
-  constexpr int NT = TS * TEAMS;       // CTA threads
+  constexpr int NTI = TS * TEAMS;      // recompute threads
+  constexpr int NT = NTI + 32 * SW;    // CTA threads
   constexpr int NWT = TS / 32;         // warps per team
   constexpr int NW = NT / 32;
+  constexpr int GPL = NV * TS / 32;    // stream lanes: float4 column groups lane + 32 i
   constexpr int XS = Geo<D>::XS, SLOT = Geo<D>::SLOT;
   constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;   // fp32 partial over <= 32 rows
   constexpr int LPR = 32 / TR;                                   // lanes per row after the transpose-reduce
@@ -91,16 +100,19 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   constexpr int PER = NWT / G;                                   // partials summed per lane
   static_assert(TEAMS >= 1 && TEAMS <= 4, "1 to 4 teams");
   static_assert(TR * G <= 32 && NWT % G == 0, "exchange layout");
-  __shared__ __align__(16) Smem<TS, TEAMS, TR> S;
+  __shared__ __align__(16) Smem<TS, TEAMS, TR, NW, SW> S;
   // dynamic: fp64 accumulators [NV*4][NT] (element-major: consecutive threads, consecutive
   // words), then the tile slots [TEAMS][kRing][SLOT]
   extern __shared__ double acc_dyn[];
   double (*acc_s)[NT] = reinterpret_cast<double (*)[NT]>(acc_dyn);
   float* slots = reinterpret_cast<float*>(acc_dyn + NV * 4 * NT);
   float4* s_sm = reinterpret_cast<float4*>(slots + TEAMS * kRing * SLOT);   // [NV * TS] s in fp32
+  double* sacc0 = reinterpret_cast<double*>(s_sm + NV * TS);   // [SW][GPL * 4][32] stream partials
+  float* sring0 = reinterpret_cast<float*>(sacc0 + SW * GPL * 4 * 32);   // [SW][kSRing][kSRow]
 
   const int tid = threadIdx.x;
-  const int team = tid / TS, ttid = tid - team * TS;
+  const bool strm = SW > 0 && tid >= NTI;   // a stream warp
+  const int team = strm ? TEAMS : tid / TS, ttid = strm ? tid - NTI : tid - team * TS;
   const int warp = tid >> 5, lane = tid & 31;
   const int twarp = ttid >> 5;          // warp index within the team
   const uint32_t team_bar = 2u + (uint32_t)team;   // named barrier ids 2..5 (1 = whole CTA)
@@ -114,6 +126,10 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     for (int tm = 0; tm < TEAMS; ++tm) {
       for (int i = 0; i < kRing; ++i) mbar_init(&S.full[tm][i], 32);
       for (int i = 0; i < 3; ++i) mbar_init(&S.redbar[tm][i], TS);
+    }
+    if constexpr (SW > 0) {
+      for (int w = 0; w < SW; ++w)
+        for (int i = 0; i < kSRing; ++i) mbar_init(&S.sfull[w][i], 1);
     }
     fence_mbar_init();
   }
@@ -193,10 +209,12 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
   int64_t rbeg[2];   // this CTA's rows of each side (pass-invariant)
   int rcnt[2];
 #pragma unroll
-  for (int fs = 0; fs < 2; ++fs) {
+  for (int fs = 0; fs < 2; ++fs) {   // hybrid: the recompute rows follow the streamed prefix
+    const int64_t ns = SW > 0 ? A.nstream[fs] : 0;
     int64_t q1;
-    cta_rows(A.rows[fs], A.gpp, cta, &rbeg[fs], &q1);
+    cta_rows(A.rows[fs] - ns, A.gpp, cta, &rbeg[fs], &q1);
     rcnt[fs] = (int)(q1 - rbeg[fs]);
+    rbeg[fs] += ns;
   }
   auto make_feed = [&](int q) {
     const int kq = pass_kind(q, A);
@@ -234,6 +252,127 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     else cp_async_commit();
   };
   bool prefetched = false;   // this pass's first kAhead tiles were issued by the previous pass
+  uint32_t skw = 0;           // hybrid: rows this stream warp has consumed (ring slot / parity)
+
+  // Stream warps (hybrid): warp sw takes rows sb0 + sw, + SW, ... of this CTA's share of the
+  // streamed prefix.  Its lane 0 keeps kSRing rows in flight with 1-D bulk copies (TMA engine)
+  // into the warp's own ring (completion: the slot's mbarrier tx count); the warp reads a row
+  // from shared memory (lane: float4 groups lane + 32 i), refills the slot, forms the dot with
+  // s as a lane partial plus a fixed xor butterfly (every lane gets the same bits), then
+  // w_j = c_j / t_j and the fp32 accumulation F_j w_j, flushed to the warp's fp64 partials
+  // every 32 rows.  The features are the materialised ones (h_j included), so the init pass
+  // accumulates with u^0 = 1.
+  auto stream_pass = [&](int kind, int f, int p) {
+    if constexpr (SW > 0) {
+      const int sw = ttid >> 5;
+      double* sacc = sacc0 + sw * (GPL * 4 * 32);
+      float* ring = sring0 + sw * (kSRing * kSRow);
+      const bool kDot = kind != PK_INIT, kAcc = kind != PK_ERR;
+      const bool kOut = kind == PK_U || kind == PK_V;
+      int64_t sb0, sb1;
+      cta_rows(A.nstream[f], A.gpp, cta, &sb0, &sb1);
+      // this warp's rows: sb0 + sw + SW k, k < K (one bulk copy each into its ring)
+      const int K = (sb1 - sb0 > sw) ? (int)((sb1 - sb0 - sw + SW - 1) / SW) : 0;
+      const float* Fp = A.F[f];
+      const float* wp = A.w[f] + (int64_t)prob * A.wstride[f];
+      const bool nvo = (kind == PK_ERR) || (kind == PK_V && p >= 3);
+      const float* vold = nvo ? vbuf_ptr(A, prob, (kind == PK_ERR) ? A.T : (p + 1) / 2 - 1) : nullptr;
+      float* outp = kind == PK_U ? A.out[0] + (int64_t)prob * A.wstride[0]
+                                 : (kind == PK_V ? vbuf_ptr(A, prob, (p + 1) / 2) : nullptr);
+      const uint32_t rowbytes = (uint32_t)r * 4u;
+      const uint32_t k0 = skw;
+      auto issue = [&](int k) {   // lane 0
+        const uint32_t slot = (k0 + (uint32_t)k) % kSRing;
+        mbar_arrive_expect_tx(&S.sfull[sw][slot], rowbytes);
+        bulk_g2s(ring + slot * kSRow, Fp + (sb0 + sw + (int64_t)SW * k) * r, rowbytes,
+                 &S.sfull[sw][slot], policy_evict_first());
+      };
+      if (lane == 0)
+        for (int k = 0; k < K && k < kSRing; ++k) issue(k);
+      float4 sv[GPL], acc[GPL];
+#pragma unroll
+      for (int i = 0; i < GPL; ++i) {
+        const int g = lane + 32 * i;
+        sv[i] = (kDot && g < R4) ? s_sm[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int e = lane; e < GPL * 4 * 32; e += 32) sacc[e] = 0.0;
+      auto flush = [&]() {
+#pragma unroll
+        for (int i = 0; i < GPL; ++i) {
+          sacc[(i * 4 + 0) * 32 + lane] += (double)acc[i].x;
+          sacc[(i * 4 + 1) * 32 + lane] += (double)acc[i].y;
+          sacc[(i * 4 + 2) * 32 + lane] += (double)acc[i].z;
+          sacc[(i * 4 + 3) * 32 + lane] += (double)acc[i].w;
+          acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      double errw = 0.0, brkw = 0.0;
+      float creg = 0.f, vreg = 0.f;   // c_j, v_old_j of rows k0..k0+31 (lane l: row k0 + l)
+      for (int k = 0; k < K; ++k) {
+        if ((k & 31) == 0) {
+          const int kk = k + lane;
+          const int64_t j = sb0 + sw + (int64_t)SW * kk;
+          creg = kk < K ? __ldg(wp + j) : 0.f;
+          vreg = (kk < K && nvo) ? __ldcg(vold + j) : 0.f;
+        }
+        const float cj = __shfl_sync(0xffffffffu, creg, k & 31);
+        const float vo = __shfl_sync(0xffffffffu, vreg, k & 31);
+        const int64_t j = sb0 + sw + (int64_t)SW * k;
+        const uint32_t gk = k0 + (uint32_t)k;
+        mbar_wait(&S.sfull[sw][gk % kSRing], (gk / kSRing) & 1u);
+        const float* row = ring + (gk % kSRing) * kSRow;
+        float4 fr[GPL];
+#pragma unroll
+        for (int i = 0; i < GPL; ++i) {
+          const int g = lane + 32 * i;
+          fr[i] = g < R4 ? lds128(row + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        if (lane == 0 && k + kSRing < K) {   // the slot is free again: refill it
+          fence_proxy_async_smem();
+          issue(k + kSRing);
+        }
+        float w = 1.f;
+        if (kDot) {
+          float2 pp = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < GPL; ++i) {
+            pp = fma2(make_float2(fr[i].x, fr[i].y), make_float2(sv[i].x, sv[i].y), pp);
+            pp = fma2(make_float2(fr[i].z, fr[i].w), make_float2(sv[i].z, sv[i].w), pp);
+          }
+          float t = pp.x + pp.y;
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+          w = cj * rcp_approx(t);   // w_j = c_j / t_j (as the recompute teams)
+          if (lane == 0) {
+            if (nvo) errw += fabs((double)vo * (double)t - (double)cj);
+            if (kOut) {
+              if (!(w > 0.f) || !isfinite(w)) brkw += 1.0;
+              outp[j] = w;
+            }
+          }
+          if (!kAcc) w = 0.f;
+        }
+        if (kAcc) {
+          const float2 w2 = make_float2(w, w);
+#pragma unroll
+          for (int i = 0; i < GPL; ++i) {
+            const float2 lo = fma2(make_float2(fr[i].x, fr[i].y), w2, make_float2(acc[i].x, acc[i].y));
+            const float2 hi = fma2(make_float2(fr[i].z, fr[i].w), w2, make_float2(acc[i].z, acc[i].w));
+            acc[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
+          }
+          if ((k & 31) == 31) flush();
+        }
+      }
+      skw += (uint32_t)K;
+      if (kAcc) flush();
+      if (lane == 0) {
+        S.xsS[0][sw] = errw;
+        S.xsS[1][sw] = brkw;
+      }
+    }
+  };
 
   for (int p = A.pass_begin;; ++p) {
     // ---------------- results of pass q = p-1: stopping test (see lsk_sinkhorn.cu) -------
@@ -372,11 +511,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
               float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);   // STAB: al2 = -m_j
 #pragma unroll
               for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
-#ifdef LSK_ABL_EX2
-              fr[i][j][h] = e;
-#else
               fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
-#endif
             }
           }
         }
@@ -393,20 +528,14 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
             }
             pr[i] = pp.x + pp.y;
           }
-#ifdef LSK_ABL_XCH
-          const float tot = pr[lane % TR];
-#else
           const float tot = warp_transpose_reduce<TR>(pr, lane);
-#endif
           if ((lane & (LPR - 1)) == 0) S.red[team][rb][lane / LPR][twarp] = tot;
         }
         if constexpr (PIPE) {
           mbar_arrive(&S.redbar[team][rb]);   // also the per-tile team sync of the init pass
         } else {
           if (twarp == 0) cp_async_wait<kAhead - 1>();   // tile t+1 landed
-#ifndef LSK_ABL_BAR
           named_bar(team_bar, TS);   // publishes red[rb] and slot t+1 to the team
-#endif
         }
       };
 
@@ -500,13 +629,17 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
         }
       }
     };
-    switch (kind) {
-      case PK_INIT: run_tiles(std::integral_constant<int, PK_INIT>{}); break;
-      case PK_V: run_tiles(std::integral_constant<int, PK_V>{}); break;
-      case PK_U: run_tiles(std::integral_constant<int, PK_U>{}); break;
-      default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
+    if (strm) {
+      stream_pass(kind, f, p);
+    } else {
+      switch (kind) {
+        case PK_INIT: run_tiles(std::integral_constant<int, PK_INIT>{}); break;
+        case PK_V: run_tiles(std::integral_constant<int, PK_V>{}); break;
+        case PK_U: run_tiles(std::integral_constant<int, PK_U>{}); break;
+        default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
+      }
+      gt += (uint32_t)ntiles;
     }
-    gt += (uint32_t)ntiles;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       acc_s[j * 4 + 0][tid] += (double)acc32[j].x;
@@ -517,24 +650,24 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
 
     // ---------------- end of pass: teams combined (fixed order), cross-CTA fp64 reduction ---
     double e0 = 0.0, e1 = 0.0;
-    if (twarp == NWT - 1) {
+    if (!strm && twarp == NWT - 1) {
       e0 = warp_sum_f64(S.errL[team][lane]);
       e1 = warp_sum_f64(S.brkL[team][lane]);
       S.errL[team][lane] = 0.0;
       S.brkL[team][lane] = 0.0;
     }
-    if (twarp == NWT - 1 && lane == 0) {   // hand the team's extras to its thread 0
+    if (!strm && twarp == NWT - 1 && lane == 0) {   // hand the team's extras to its thread 0
       S.xs[0][NW - 1 - team] = e0;
       S.xs[1][NW - 1 - team] = e1;
     }
     named_bar(1, NT);
-    if (ttid == 0) {
+    if (!strm && ttid == 0) {
       e0 = S.xs[0][NW - 1 - team];
       e1 = S.xs[1][NW - 1 - team];
     }
     named_bar(1, NT);
     if constexpr (TEAMS > 1) {
-      if (team > 0 && ttid == 0) {
+      if (!strm && team > 0 && ttid == 0) {
         S.xs[0][team] = e0;
         S.xs[1][team] = e1;
       }
@@ -547,6 +680,27 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
           if (ttid == 0) {
             e0 += S.xs[0][tm];
             e1 += S.xs[1][tm];
+          }
+        }
+      }
+      named_bar(1, NT);
+    }
+    if constexpr (SW > 0) {   // then the stream warps' partials, warp 0, 1, ... (fixed order)
+      if (team == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          const int gg = ttid + j * TS;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double a = acc_s[j * 4 + q][ttid];
+            for (int w = 0; w < SW; ++w) a += sacc0[w * (GPL * 4 * 32) + ((gg >> 5) * 4 + q) * 32 + (gg & 31)];
+            acc_s[j * 4 + q][ttid] = a;
+          }
+        }
+        if (ttid == 0) {
+          for (int w = 0; w < SW; ++w) {
+            e0 += S.xsS[0][w];
+            e1 += S.xsS[1][w];
           }
         }
       }
@@ -584,7 +738,7 @@ __global__ void __launch_bounds__(TS * TEAMS, 1) implicit_kernel(const SinkArgs 
     if constexpr (!PIPE) {
       const int q = p + 1;
       if (q < A.pass_end && pass_kind(q, A) != PK_NONE) {
-        if (twarp == 0) {
+        if (!strm && twarp == 0) {
           const Feed nf = make_feed(q);
 #pragma unroll
           for (int t = 0; t < kAhead; ++t) issue_tile(nf, gt, t);
@@ -715,10 +869,11 @@ __global__ void __launch_bounds__(256) row_shift_kernel(const float* __restrict_
   A[j] = ((double)(al * c2) + (double)mx) * 0.69314718055994530942;
 }
 
-template <int TS, int TEAMS, int NV, int TR, int D>
+template <int TS, int TEAMS, int NV, int TR, int D, int SW = 0>
 constexpr size_t dyn_smem() {
-  return sizeof(double) * NV * 4 * TS * TEAMS + sizeof(float) * TEAMS * kRing * Geo<D>::SLOT +
-         sizeof(float4) * NV * TS;
+  return sizeof(double) * NV * 4 * (TS * TEAMS + 32 * SW) +
+         sizeof(float) * TEAMS * kRing * Geo<D>::SLOT + sizeof(float4) * NV * TS +
+         sizeof(double) * SW * NV * TS * 4 + sizeof(float) * SW * kSRing * kSRow;
 }
 
 }  // namespace impl
@@ -774,31 +929,44 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_EXTRA(X)
 #endif
 
-template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE>
+template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
-  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE>;
-  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE, SW>;
+  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>();
+  constexpr int nthr = TS * TM + 32 * SW;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   if (coop) {
     void* args[] = {(void*)&a};
-    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(TS * TM), args, dyn, s);
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nthr), args, dyn, s);
   } else {
-    kern<<<grid, TS * TM, dyn, s>>>(a);
+    kern<<<grid, nthr, dyn, s>>>(a);
     e = cudaGetLastError();
   }
   count_launch();
   return e;
 }
 
-template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE>
+template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
 static int occupancy_cfg() {
-  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE>;
-  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D>();
+  auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE, SW>;
+  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>();
   int nb = 0;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TS * TM, dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TS * TM + 32 * SW, dyn);
   return nb;
+}
+
+// Hybrid (a.nstream > 0): one 128-thread recompute team (measured 21.7 vs 20.5 us per pass for
+// the two-team default on config 2 — the team's registers are what the stream warps use) plus
+// four stream warps; r <= 1024, d <= 3, plain or factored exponent.
+static cudaError_t launch_hybrid(const SinkArgs& a, bool coop, int grid, cudaStream_t s, int* occ) {
+  if (a.r > 1024 || a.d > 3 || a.stab) return cudaErrorInvalidConfiguration;
+  const int mode = a.hrow[0] != nullptr ? 1 : 0;
+#define H(D_, M_)                                                                                if (a.d == D_ && mode == M_) {                                                                   if (occ) {                                                                                       *occ = occupancy_cfg<128, 1, 2, 16, D_, M_, false, 4>();                                       return cudaSuccess;                                                                          }                                                                                              return launch_cfg<128, 1, 2, 16, D_, M_, false, 4>(a, coop, grid, s);                        }
+  H(1, 0) H(1, 1) H(2, 0) H(2, 1) H(3, 0) H(3, 1)
+#undef H
+  return cudaErrorInvalidConfiguration;
 }
 
 // the stabilised mode is instantiated for the default (non-pipelined) configurations only
@@ -816,6 +984,7 @@ static cudaError_t stab_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t
 }
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
+  if (a.nstream[0] + a.nstream[1] > 0) return launch_hybrid(a, coop, grid, s, nullptr);
   const ImplCfg c = implicit_config(a.r, a.d);
   if (c.warp && a.stab) return cudaErrorInvalidConfiguration;   // team kernel only
   if (c.warp) return launch_implicit_warp(a, coop, grid, s, nullptr);
@@ -832,6 +1001,10 @@ cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t
 }
 
 int implicit_max_ctas_per_sm(const SinkArgs& a) {
+  if (a.nstream[0] + a.nstream[1] > 0) {
+    int occ = 0;
+    return launch_hybrid(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0;
+  }
   const ImplCfg c = implicit_config(a.r, a.d);
   if (c.warp) {
     int occ = 0;

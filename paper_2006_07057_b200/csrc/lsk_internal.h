@@ -32,7 +32,9 @@ enum PassKind { PK_INIT = 0, PK_V = 1, PK_U = 2, PK_ERR = 3, PK_NONE = 4 };
 
 struct SinkArgs {
   // factor 0 = xi side (rows n, weights a, output u); factor 1 = zeta side (m, b, v)
-  const float* F[2];       // streaming: feature matrices (rows x r)
+  const float* F[2];       // streaming: feature matrices (rows x r); hybrid implicit: the
+                           // materialised rows [0, nstream) of each side
+  int64_t nstream[2];      // hybrid implicit: rows of each side streamed instead of regenerated
   const float* X[2];       // implicit: point matrices (rows x d)
   int64_t rows[2];
   int64_t fstride[2];      // per-problem element stride of F (or X) for batched

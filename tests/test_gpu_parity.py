@@ -148,6 +148,8 @@ def test_config2_reduced_ragged(L, variant):
     (2, 4099, 3907, 200, {"LSK_IWARP": "1"}),                   # warp-private kernel (8,8,1)
     (2, 4099, 3907, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,8,2"}),
     (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,8,1"}),         # lag-one pipeline
+    (2, 8011, 7993, 200, {"LSK_HYB": "0.3"}),                   # hybrid: 30% of rows streamed
+    (2, 8011, 7993, 200, {"LSK_HYB": "0.6"}),
     (5, 6151, 6143, 40, {}),                                    # team kernel (256,1,4,8)
     (5, 6151, 6143, 40, {"LSK_ICFG": "512,1,2,4,0"}),
     (5, 6151, 6143, 40, {"LSK_ICFG": "256,1,4,2,1"}),
@@ -158,7 +160,9 @@ def test_config2_reduced_ragged(L, variant):
 def test_implicit_exponent_forms_and_configs(L, monkeypatch, fact, cfg_key, n, m, T, env):
     """The implicit kernels' factored exponent (LSK_FACT=1, DESIGN.md §6 K5) and the plain
     expanded form (LSK_FACT=0), for the default and every instantiated tuning configuration
-    of the warp-private and the team kernel, against the oracle (ragged n, m: tail tiles)."""
+    of the warp-private and the team kernel, and the hybrid kernel (LSK_HYB: materialised
+    rows streamed by extra warps of the same launch), against the oracle (ragged n, m: tail
+    tiles)."""
     monkeypatch.setenv("LSK_FACT", fact)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
