@@ -57,7 +57,7 @@ struct SinkArgs {
   int multi_launch;        // 1: one pass per launch (NCCL all-reduce of svec between launches)
   int nstage;              // ring stages
   int stage_floats;        // floats per stage (header + TR*r for streaming)
-  double* part;            // [nprob][(r+kExtra) * gpp] column-major partials
+  double* part;            // [nprob][(r+kExtra+4)/4 blocks][gpp][4] fp64 partials (lsk_sink_common.cuh)
   double* svec;            // [nprob][r+kExtra]
   unsigned int* bar;       // [nprob] monotone barrier counters (zeroed once per solve)
   double* state;           // [nprob][kStateDoubles]
@@ -92,7 +92,8 @@ void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv);
 size_t sinkhorn_static_smem();
 int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t dyn_smem);
 
-// Implicit (recompute) kernel (lsk_implicit.cu): all-consumer CTAs, software-pipelined tiles.
+// Implicit (recompute) kernel (lsk_implicit.cu): teams of recompute threads (per-team tile
+// barrier; optional lag-one pipeline), optional stream warps (hybrid, LSK_HYB).
 struct ImplCfg {
   int ts, teams, nv, tr, pipe;
   int warp;   // 1: warp-private kernel (lsk_implicit_warp.cu, r <= 1024)
