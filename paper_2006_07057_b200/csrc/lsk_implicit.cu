@@ -22,7 +22,8 @@
 // column: thread t of a team owns float4 column groups {t, t+TS, ...} (its W, beta2, slice of
 // s and fp32 accumulators live in registers; the fp64 accumulators in shared memory).  Teams
 // take alternate tiles of TR rows of the CTA's row range.  Each team's warp 0 stages tiles
-// (point rows, c_j, h_j, v_old_j) kAhead = 8 tiles ahead with cp.async into a 16-slot ring.
+// (point rows, c_j, h_j, v_old_j) kAhead = 2 tiles ahead with cp.async into an 8-slot ring
+// (measured: 16 slots 8 ahead 20.3 us/pass on config 2, 32 / 16 21.0, 8 / 2 20.1).
 //
 // Per tile (default, PIPE = 0): features -> row-dot partials -> warp transpose-reduce -> one
 // named barrier per team (publishes the partials and the next slot) -> the exchange: row i's
@@ -46,10 +47,10 @@ namespace lsk {
 
 namespace impl {
 
-constexpr int kRing = 16;   // tile slots per team
+constexpr int kRing = 8;    // tile slots per team
 constexpr int kSRing = 6;   // hybrid: row slots per stream warp (bulk copies in flight)
 constexpr int kSRow = 1024; // hybrid: floats per row slot (r <= 1024)
-constexpr int kAhead = 8;   // the loader stages tile t+kAhead when tile t starts (<= kRing/2)
+constexpr int kAhead = 2;   // the loader stages tile t+kAhead when tile t starts (<= kRing/2)
 
 template <int D>
 struct Geo {
