@@ -91,3 +91,15 @@ def test_argument_validation_without_gpu():
                                       ctypes.byref(o), None, None, ctypes.byref(rep), None, None)
     assert st == -1
     assert "multiple of 4" in L._lib.lsk_last_error().decode()
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """The product path has no CPU fallback: importing the binding with no CUDA library
+    raises instead of degrading (the tuning override points at a file that does not exist)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, LSK_LIB_PATH=str(tmp_path / "missing_liblsk.so"))
+    res = subprocess.run([sys.executable, "-c", "import paper_2006_07057_b200"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode != 0
+    assert "ImportError" in res.stderr and "no CPU fallback" in res.stderr
