@@ -31,6 +31,12 @@ Pins (tests/test_oracle_*.py) — every function below is pinned to something ou
                         rank-one closed forms; weak duality at every iterate; accepted
                         L <= 4 (phi is 2-smooth); plan marginals -> (a, b), unit mass
                         (tests/test_oracle_accel.py)
+  max_norm              hand-computed norms of Pythagorean triples, max in X or in Y
+  marginal_error        a 2x2 case worked by hand (tests/test_oracle_sinkhorn.py)
+  C29 allowance         without it the accepted L leaves the smoothness bound 4 in the
+                        rounding regime; with it L <= 4 (tests/test_oracle_accel.py)
+  matrix_free.py + lsk_oracle_mf.c (config 5's full-size oracle) == the materialised numpy
+                        oracle; rank-one closed form at n = 2e5; P9 (test_oracle_matrix_free.py)
   exact gaussian ROT    paper RE behaviour on the Fig. 1 setup (P16, qualitative: the
                         paper prints no numbers — "parity unpinned" for the RE values
                         themselves; only the sign/monotonic trends are asserted)
@@ -403,7 +409,8 @@ def feature_matrix_arccos(X, U, sigma: float, s: int, kappa: float) -> np.ndarra
 def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
                          Kt_mv: Callable[[np.ndarray], np.ndarray],
                          a, b, eps: float, L0: float = 1.0, T: Optional[int] = None,
-                         tol: Optional[float] = None, max_iter: int = 100000) -> dict:
+                         tol: Optional[float] = None, max_iter: int = 100000,
+                         allowance: float = 1e-13, max_trials: int = 2000) -> dict:
     """Alg. 2 step by step, with the readings of DESIGN.md C22-C27:
       C22  phi(eta) := -F_theta(eta)/eps = log<e^{eta1}, K e^{eta2}> - <eta1,a> - <eta2,b>
            is the objective minimised; Eq. (dual-smooth)'s "<K e^{eta2}>" is <e^{eta1}, K e^{eta2}>.
@@ -465,7 +472,7 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
                 new1 = lam1
                 new2 = lam2 + np.log(b) - np.log(np.exp(lam2) * Ktu)
             ph_lam = phi(lam1, lam2)
-            if phi(new1, new2) <= ph_lam - (n1 + n2) / (2.0 * L1) + 1e-13 * max(1.0, abs(ph_lam)):
+            if phi(new1, new2) <= ph_lam - (n1 + n2) / (2.0 * L1) + allowance * max(1.0, abs(ph_lam)):
                 zet1 = zet1 - a1 * g1                                   # C26
                 zet2 = zet2 - a1 * g2
                 # x_hat^{k+1} = (a_{k+1} c^{-1} z + L_k a_k^2 x_hat^k) / (L_{k+1} a_{k+1}^2)
@@ -475,6 +482,8 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
                 ak, Lk = a1, L1
                 break
             L1 = 2.0 * L1
+            if trials >= max_trials:
+                raise RuntimeError("Alg. 2 line search: %d rejected trials (L = %g)" % (trials, L1))
         it += 1
         F_tr.append(-eps * phi(eta1, eta2))
         L_tr.append(Lk)
@@ -491,12 +500,13 @@ def accelerated_sinkhorn(K_mv: Callable[[np.ndarray], np.ndarray],
 
 
 def accelerated_sinkhorn_factored(xi: np.ndarray, zeta: np.ndarray, a, b, eps: float,
-                                  L0: float = 1.0, T=None, tol=None, max_iter=100000) -> dict:
+                                  L0: float = 1.0, T=None, tol=None, max_iter=100000,
+                                  **kw) -> dict:
     """Alg. 2 on K_theta = xi^T zeta: every K application costs r(n+m)."""
     xi = np.asarray(xi, dtype=np.float64)
     zeta = np.asarray(zeta, dtype=np.float64)
     return accelerated_sinkhorn(lambda v: xi.T @ (zeta @ v), lambda u: zeta.T @ (xi @ u), a, b,
-                                eps, L0, T, tol, max_iter)
+                                eps, L0, T, tol, max_iter, **kw)
 
 
 # ---------------------------------------------------------------------------------------

@@ -83,3 +83,26 @@ def test_accel_tolerance_mode_stops_on_plan_marginals():
     assert np.abs(res["p1"] - a).sum() + np.abs(res["p2"] - b).sum() < 1e-3
     again = O.accelerated_sinkhorn_factored(xi, zeta, a, b, eps, T=res["iters"] - 1)
     assert np.abs(again["p1"] - a).sum() + np.abs(again["p2"] - b).sum() >= 1e-3
+
+
+@pytest.mark.parametrize("seed,n,m,r,eps", [(13, 8, 8, 5, 0.5), (17, 8, 8, 5, 0.5),
+                                            (18, 23, 31, 7, 0.1)])
+def test_accel_rounding_allowance_keeps_L_within_smoothness_bound(seed, n, m, r, eps):
+    """Reading C29.  phi is 2-smooth, so in exact arithmetic every L >= 2 passes the acceptance
+    test of the exact block step and no accepted L exceeds 4.  Run into the rounding regime
+    (|grad phi|^2 ~ 1e-19: the required decrease |grad|^2/(2L) is below the fp64 rounding of
+    phi itself),
+    the strict test (allowance 0) rejects steps on rounding noise alone and doubles L past the
+    bound (to 2^12 and beyond on these instances); with the 1e-13 max(1,|phi|) allowance every
+    accepted L stays <= 4 and the value is unchanged."""
+    prob, xi, zeta, _ = _small_factored(seed, n, m, r, eps=eps)
+    a, b = prob["a"].astype(np.float64), prob["b"].astype(np.float64)
+    a, b = a / a.sum(), b / b.sum()
+    strict = O.accelerated_sinkhorn_factored(xi, zeta, a, b, eps, T=4000, allowance=0.0)
+    k = int(np.argmax(strict["L_trace"] > 4.0))
+    assert strict["L_trace"].max() > 4.0 * 2 ** 8                  # the bound is violated ...
+    phi_k = abs(strict["F_trace"][k]) / eps                        # ... only in the rounding regime
+    assert strict["grad_norms"][k].sum() / 2.0 < 4.0 * 2.0 ** -52 * max(1.0, phi_k)
+    kept = O.accelerated_sinkhorn_factored(xi, zeta, a, b, eps, T=4000)
+    assert kept["L_trace"].max() <= 4.0
+    assert abs(kept["F"] - strict["F"]) <= 1e-14 * abs(kept["F"])

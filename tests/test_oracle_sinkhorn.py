@@ -244,3 +244,32 @@ def test_envelope_gradients_finite_differences():
             args_p[name], args_m[name] = P, M
             fd = (W(args_p["X"], args_p["Y"], args_p["U"]) - W(args_m["X"], args_m["Y"], args_m["U"])) / (2 * h)
             assert abs(fd - grad[i, c]) <= 1e-6 * max(1.0, abs(fd)), (name, i, c, fd, grad[i, c])
+
+
+# ---------------- hand-computed pins of the two helpers ---------------------------------------
+def test_max_norm_hand_computed():
+    """R = max over BOTH clouds of |p|_2 (reading C3), with Pythagorean triples (exact in fp32
+    and fp64): the maximum in Y, then in X, then with negative coordinates and d = 3."""
+    X = np.array([[3.0, 4.0], [0.0, 1.0]], np.float32)            # norms 5, 1
+    Y = np.array([[6.0, 8.0], [-1.0, 0.0]], np.float32)           # norms 10, 1
+    assert O.max_norm(X, Y) == 10.0
+    assert O.max_norm(Y[1:], X) == 5.0
+    X3 = np.array([[-3.0, 4.0, 12.0], [1.0, 2.0, 2.0]], np.float32)   # 13, 3
+    Y3 = np.array([[2.0, -3.0, 6.0]], np.float32)                      # 7
+    assert O.max_norm(X3, Y3) == 13.0
+    assert O.max_norm(Y3, X3[1:]) == 7.0
+
+
+def test_marginal_error_hand_computed():
+    """|v o K^T u - b|_1 on a 2 x 2 case worked by hand:
+    K = [[1,2],[3,4]], u = (1,2): K^T u = (7, 10); v = (1/2, 1/4): v o K^T u = (3.5, 2.5);
+    b = (0.4, 0.6): |(3.1, 1.9)|_1 = 5.0.  A v with the opposite sign of error: v = (0, 0.1)
+    gives |(-0.4, 0.4)|_1 = 0.8."""
+    K = np.array([[1.0, 2.0], [3.0, 4.0]])
+    u = np.array([1.0, 2.0])
+    b = np.array([0.4, 0.6])
+    assert abs(O.marginal_error(u, np.array([0.5, 0.25]), K.T @ u, b) - 5.0) < 1e-15
+    assert abs(O.marginal_error(u, np.array([0.0, 0.1]), K.T @ u, b) - 0.8) < 1e-15
+    # and the oracle's recorded err_t is this quantity of its own iterates
+    res = O.sinkhorn_dense(K, [0.5, 0.5], [0.4, 0.6], T=3, record_err=True)
+    assert abs(res["errs"][-1] - O.marginal_error(res["u"], res["v"], K.T @ res["u"], [0.4, 0.6])) == 0.0
