@@ -25,6 +25,11 @@
  *     synchronise `stream` before returning.
  *   - Errors: a negative lsk_status; lsk_last_error() returns a thread-local message.  No
  *     C++ exception crosses the ABI.  On error, outputs are unspecified.
+ *   - Asynchronous solve errors (a solve called with rep == NULL does not synchronise): a
+ *     zero / non-finite row dot (LSK_EBREAKDOWN), a weight that is not finite and > 0
+ *     (LSK_EWEIGHTS) and a cross-GPU exchange timeout (LSK_ENCCL) set a STICKY status of the
+ *     (device, stream).  The next synchronising call on that stream that checks it returns the
+ *     error and clears it: lsk_stream_status, lsk_rot_value, and any solve given a report.
  *   - Thread safety: calls on different streams may run concurrently; one solve at a time
  *     per (device, stream) workspace.
  */
@@ -43,7 +48,9 @@ typedef enum lsk_status {
   LSK_EINVAL = -1,         /* n,m,r,d < 1; eps <= 0; r % 4 != 0; NULL or misaligned pointer */
   LSK_EDIM = -2,           /* unsupported size combination (e.g. d > 16 for implicit)       */
   LSK_EDOMAIN = -3,        /* R given and a point lies outside B(0,R); W0 argument < -1/e   */
-  LSK_EWEIGHTS = -4,       /* reserved: weight validation failure                           */
+  LSK_EWEIGHTS = -4,       /* a weight a_i or b_j is not finite and > 0 (mu, nu are probability
+                              measures with positive masses; checked by the
+                              solve kernels on every row they read: report or sticky status) */
   LSK_EBREAKDOWN = -5,     /* a row dot K v or K^T u was 0 / inf / nan        */
   LSK_ECUDA = -6,          /* CUDA runtime error (message in lsk_last_error)                 */
   LSK_ENCCL = -7,          /* NCCL error or NCCL library not loadable                       */
@@ -101,6 +108,10 @@ typedef struct lsk_comm lsk_comm;   /* opaque NCCL communicator; NULL = single G
 
 const char* lsk_version(void);
 const char* lsk_last_error(void);
+/* Synchronises `stream` and returns (then clears) its sticky status: LSK_OK, or the
+ * LSK_EBREAKDOWN / LSK_EWEIGHTS / LSK_ENCCL of a report-less solve enqueued on it since the
+ * last check (see Conventions). */
+lsk_status lsk_stream_status(void* stream);
 
 /* ---- a1: feature parameters (host fp64) --------------------------------------------- */
 /* Principal-branch Lambert W_0 ("W_0 is the Lambert function"); Halley
@@ -170,8 +181,11 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
                                           const lsk_solve_opts* o, float* u, float* v,
                                           lsk_report* rep, lsk_comm* comm, void* stream);
 
-/* Batched: `batch` independent problems in ONE launch, one CTA (no grid barrier) per
- * problem.  Xi (batch, n, r), Zeta (batch, m, r), a/u (batch, n), b/v (batch, m);
+/* Batched: `batch` independent problems in ONE persistent launch.  The grid is made of
+ * groups of gpp CTAs (gpp chosen from n, r and the SM count; gpp = 1: no cross-CTA exchange,
+ * s stays in registers); each group loops over problems group, group + ngroups, ..., and a
+ * group with gpp > 1 sums its r-vector through global memory with a group barrier per pass.
+ * Xi (batch, n, r), Zeta (batch, m, r), a/u (batch, n), b/v (batch, m);
  * reps: host array of `batch` reports (nullable). */
 lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float* Zeta,
                                          int64_t m, int32_t r, int32_t batch, const float* a,
@@ -190,7 +204,8 @@ lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, c
                                                   void* stream);
 
 /* ---- a9: read-out W_hat = eps (a^T log u + b^T log v) in fp64 ------- */
-/* rot_host: host double (the call synchronises).  With comm, partial sums are all-reduced. */
+/* rot_host: host double (the call synchronises).  With comm, partial sums are all-reduced.
+ * Also returns (and clears) the stream's sticky status of an earlier report-less solve. */
 lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,
                          int64_t n, int64_t m, double eps, double* rot_host, lsk_comm* comm,
                          void* stream);
@@ -317,6 +332,13 @@ lsk_status lsk_comm_destroy(lsk_comm* comm);
  * hanging.  LSK_EUNSUPPORTED if peer memory cannot be mapped (the NCCL path stays in use);
  * LSK_P2P=0 in the environment disables the in-kernel exchange.  Synchronises. */
 lsk_status lsk_comm_enable_p2p(lsk_comm* comm, int32_t r_max, void* stream);
+
+/* Diagnostic: the launch plan a solve of this shape would use on the current device —
+ * gpp = CTAs per problem, grid = CTAs of the launch (grid / gpp = persistent groups; a batched
+ * solve with batch > grid / gpp loops each group over several problems).  variant 1 = factor
+ * stream (lsk_factored_sinkhorn[_batched]), 2 = recompute (lsk_factored_sinkhorn_implicit*). */
+lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
+                          int32_t variant, int32_t* gpp, int32_t* grid);
 
 /* Number of kernels the library launched on this thread since the last reset (for the
  * bench's gpu_launches claim). */

@@ -71,6 +71,8 @@ _SIGS = {
     "lsk_version": (ctypes.c_char_p, []),
     "lsk_last_error": (ctypes.c_char_p, []),
     "lsk_launch_count": (c_i64, [c_i32]),
+    "lsk_stream_status": (c_i32, [ctypes.c_void_p]),
+    "lsk_solve_plan": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, P(c_i32), P(c_i32)]),
     "lsk_lambert_w0": (c_i32, [ctypes.c_double, P(ctypes.c_double)]),
     "lsk_feature_params_init": (c_i32, [ctypes.c_double, c_i32, c_i32, ctypes.c_double,
                                         ctypes.c_uint64, c_f32p, c_i64, c_f32p, c_i64,
@@ -167,6 +169,21 @@ def _check(status: int, where: str) -> int:
 
 def version() -> str:
     return _lib.lsk_version().decode()
+
+
+def lsk_stream_status(stream=None) -> int:
+    """Synchronise the stream and raise the sticky error (LSK_EBREAKDOWN / LSK_EWEIGHTS /
+    LSK_ENCCL) of a report-less solve enqueued on it; clears it (include/lsk.h Conventions)."""
+    return _check(_lib.lsk_stream_status(_stream(stream)), "lsk_stream_status")
+
+
+def lsk_solve_plan(n: int, m: int, r: int, d: int, batch: int = 1, variant: str = "stream"):
+    """(gpp, grid) of the launch a solve of this shape uses (diagnostic; include/lsk.h)."""
+    g, gr = c_i32(), c_i32()
+    _check(_lib.lsk_solve_plan(int(n), int(m), int(r), int(d), int(batch),
+                               1 if variant == "stream" else 2, ctypes.byref(g), ctypes.byref(gr)),
+           "lsk_solve_plan")
+    return g.value, gr.value
 
 
 def launch_count(reset: bool = False) -> int:

@@ -10,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include <nccl.h>
@@ -40,6 +41,18 @@ static lsk_status fail(lsk_status st, const std::string& msg) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Tuning knobs (LSK_GPP, LSK_ICFG, ...) exist only in tuning builds (-DLSK_TUNING,
+// scripts/build_variant.sh): the product library never reads them, so nothing in the
+// environment can change the kernel that runs.
+static const char* tuning_env(const char* name) {
+#ifdef LSK_TUNING
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 // ------------------------------------------------------------------ device properties ---
 static int num_sms() {
   static std::mutex mu;
@@ -62,18 +75,57 @@ static int max_smem_optin() {
 }
 
 // ------------------------------------------------------------------ workspace cache -----
+// Two growable buffers per (device, stream): slot 0 for the caller-level carve (anchor
+// constants, row factors, scratch), slot 1 for the solve state that run_solve sizes AFTER
+// planning (fp64 CTA partials for the planned number of CTAs, r-vectors, barrier counters,
+// state blocks, second v buffer) — growing slot 1 never invalidates slot-0 pointers.  Plus
+// one never-moving device int: the sticky status word (StickyBits).
 struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
 static std::mutex g_ws_mu;
-static std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+static std::map<std::tuple<int, cudaStream_t, int>, Workspace> g_ws;
+static std::map<std::pair<int, cudaStream_t>, int*> g_sticky;
 
-static lsk_status get_ws(cudaStream_t s, size_t bytes, char** out) {
+static lsk_status get_sticky(cudaStream_t s, int** out) {
   int dev = 0;
   LSK_CU(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Workspace& w = g_ws[{dev, s}];
+  int*& p = g_sticky[{dev, s}];
+  if (!p) {
+    if (cudaMalloc(&p, 256) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return fail(LSK_ENOMEM, "status word cudaMalloc failed");
+    }
+    if (cudaMemset(p, 0, 256) != cudaSuccess) return fail(LSK_ECUDA, "status word memset failed");
+  }
+  *out = p;
+  return LSK_OK;
+}
+
+// read and clear the sticky status of stream s (synchronises s); returns the status it encodes
+static lsk_status take_sticky(cudaStream_t s) {
+  int* dp;
+  LSK_TRY(get_sticky(s, &dp));
+  int bits = 0;
+  LSK_CU(cudaMemcpyAsync(&bits, dp, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LSK_CU(cudaStreamSynchronize(s));
+  if (bits == 0) return LSK_OK;
+  LSK_CU(cudaMemsetAsync(dp, 0, sizeof(int), s));
+  if (bits & STICKY_XERR)
+    return fail(LSK_ENCCL, "an earlier solve on this stream: cross-GPU peer exchange timed out");
+  if (bits & STICKY_WEIGHTS)
+    return fail(LSK_EWEIGHTS, "an earlier solve on this stream: a weight a_i or b_j is not finite and > 0");
+  return fail(LSK_EBREAKDOWN, "an earlier solve on this stream: zero or non-finite row dot");
+}
+
+static lsk_status get_ws(cudaStream_t s, size_t bytes, char** out, int slot = 0) {
+  int dev = 0;
+  LSK_CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& w = g_ws[{dev, s, slot}];
   if (w.bytes < bytes) {
     if (w.ptr) {
       cudaStreamSynchronize(s);
@@ -208,7 +260,7 @@ static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o,
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
     const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
     c->gpp = (int)std::min<int64_t>((int64_t)num_sms() * cps, want);
-    if (const char* e = getenv("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
+    if (const char* e = tuning_env("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
     c->coop = c->gpp > 1;
   }
@@ -222,7 +274,7 @@ static lsk_status setup_fact(SinkArgs& A, double R, int batch, cudaStream_t s, c
                              Carve& cv) {
   A.hrow[0] = A.hrow[1] = nullptr;
   A.abar = 0.f;
-  const char* e = getenv("LSK_FACT");
+  const char* e = tuning_env("LSK_FACT");
   if (e && atoi(e) == 0) return LSK_OK;
   const double span = 1.4426950408889634074 / A.eps * R * R;
   if (!(R > 0.0) || !(span <= 60.0)) return LSK_OK;
@@ -256,7 +308,7 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   if (nv > 8) return fail(LSK_EDIM, "r too large for this variant");
   // the pipelined tile loop holds two stages while the producer fills a third
   if (nst < 3) return fail(LSK_EDIM, "r too large: three ring stages do not fit in shared memory");
-  if (const char* e = getenv("LSK_NSTAGE")) nst = std::max(3, std::min(nst, atoi(e)));   // tuning knob
+  if (const char* e = tuning_env("LSK_NSTAGE")) nst = std::max(3, std::min(nst, atoi(e)));   // tuning knob
   A.tr = tr;
   A.nv = nv;
   c->stage_floats = sf;
@@ -287,7 +339,8 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
                          (gsz == 1 ? 1.0 : t_pass / (t_pass + 6.4e-6));
       if (eff > best_eff + 1e-9) { best_eff = eff; best_g = gsz; }
     }
-    if (const char* e = getenv("LSK_BGPP")) best_g = std::max(1, atoi(e));   // tuning knob
+    if (const char* e = tuning_env("LSK_BGPP"))   // tuning knob, clamped to what the grid holds
+      best_g = std::max(1, std::min(atoi(e), std::min(64, slots)));
     c->gpp = best_g;
     const int ngroups = std::min(slots / best_g, batch);
     c->grid = ngroups * best_g;
@@ -296,7 +349,7 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
     const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
     c->gpp = (int)std::min<int64_t>((int64_t)sms * cps, want);
-    if (const char* e = getenv("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
+    if (const char* e = tuning_env("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
     c->coop = c->gpp > 1;
   }
@@ -304,8 +357,7 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
 }
 
 static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_opts* o,
-                            lsk_report* reps, lsk_comm* comm, cudaStream_t s, char* ws,
-                            Carve& cv) {
+                            lsk_report* reps, lsk_comm* comm, cudaStream_t s) {
   if (!o) return fail(LSK_EINVAL, "opts is NULL");
   if (o->max_iters < 1) return fail(LSK_EINVAL, "max_iters < 1");
   A.T = o->max_iters;
@@ -334,24 +386,34 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     A.xtimeout_ns = 20LL * 1000 * 1000 * 1000;
   }
   A.gpp = c.gpp;
-  A.dbg = getenv("LSK_DEBUG") ? atoi(getenv("LSK_DEBUG")) : 0;
-  A.l2_resident = getenv("LSK_L2RES") ? (float)atof(getenv("LSK_L2RES")) : 0.f;   // tuning knob
+  A.dbg = tuning_env("LSK_DEBUG") ? atoi(tuning_env("LSK_DEBUG")) : 0;
+  A.l2_resident = tuning_env("LSK_L2RES") ? (float)atof(tuning_env("LSK_L2RES")) : 0.f;   // tuning knob
   A.nprob = batch;
   A.nstage = c.nstage;
   A.stage_floats = c.stage_floats;
   const int64_t rs = A.r + kExtra;
+  // the solve state, sized for the planned CTA count (workspace slot 1):
   // part: [batch][(r + kExtra + 4) / 4 blocks][gpp][4] (block r/4 + 1 carries the read-out
   // partials; lsk_sink_common.cuh);
   // svec: [batch][2][r + kExtra], armed with the all-ones sentinel (lsk_sink_common.cuh)
-  A.part = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * (rs + 4) * c.gpp * batch));
-  A.svec = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * 2 * rs * batch));
+  Carve sz;
+  const size_t oPart = sz.take(sizeof(double) * (rs + 4) * c.gpp * batch);
+  const size_t oSvec = sz.take(sizeof(double) * 2 * rs * batch);
+  const size_t oState = sz.take(sizeof(double) * kStateDoubles * batch);
+  const size_t oBar = sz.take(sizeof(unsigned int) * batch);
+  const size_t oVbuf = sz.take(sizeof(float) * A.rows[1] * batch);
+  char* ws;
+  LSK_TRY(get_ws(s, sz.off, &ws, 1));
+  LSK_TRY(get_sticky(s, &A.sticky));
+  A.part = reinterpret_cast<double*>(ws + oPart);
+  A.svec = reinterpret_cast<double*>(ws + oSvec);
   LSK_CU(cudaMemsetAsync(A.svec, 0xFF, sizeof(double) * 2 * rs * batch, s));
-  A.state = reinterpret_cast<double*>(ws + cv.take(sizeof(double) * kStateDoubles * batch));
-  A.bar = reinterpret_cast<unsigned int*>(ws + cv.take(sizeof(unsigned int) * batch));
-  A.vbuf1 = reinterpret_cast<float*>(ws + cv.take(sizeof(float) * A.rows[1] * batch));
+  A.state = reinterpret_cast<double*>(ws + oState);
+  A.bar = reinterpret_cast<unsigned int*>(ws + oBar);
+  A.vbuf1 = reinterpret_cast<float*>(ws + oVbuf);
   LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles * batch, s));
   unsigned long long* trace = nullptr;
-  const char* trace_path = getenv("LSK_TRACE");   // tuning only: per-pass barrier timestamps
+  const char* trace_path = tuning_env("LSK_TRACE");   // tuning only: per-pass barrier timestamps
   if (trace_path && batch == 1) {
     cudaMalloc(&trace, sizeof(unsigned long long) * 4 * (size_t)A.num_passes * c.gpp);
     cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 4 * (size_t)A.num_passes * c.gpp, s);
@@ -398,7 +460,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     std::vector<double> st((size_t)kStateDoubles * batch);
     LSK_CU(cudaMemcpyAsync(st.data(), A.state, sizeof(double) * st.size(), cudaMemcpyDeviceToHost, s));
     LSK_CU(cudaStreamSynchronize(s));
-    bool brk = false, notconv = false;
+    bool brk = false, notconv = false, wbad = false;
     for (int b = 0; b < batch; ++b) {
       const double* x = st.data() + (size_t)b * kStateDoubles;
       lsk_report& rp = reps[b];
@@ -411,12 +473,18 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       rp.breakdown = x[ST_BRK] > 0 ? 1 : 0;
       rp.reserved = 0;
       brk |= rp.breakdown != 0;
+      wbad |= x[ST_WBAD] > 0;
       notconv |= A.tol_mode && !rp.converged;
     }
+    // reported here: clear the sticky word (it also carries any earlier report-less solve)
+    const lsk_status sticky = take_sticky(s);
+    if (sticky == LSK_ECUDA || sticky == LSK_ENOMEM) return sticky;
     for (int b = 0; b < batch; ++b)
       if (st[(size_t)b * kStateDoubles + ST_XERR] != 0.0)
         return fail(LSK_ENCCL, "cross-GPU peer exchange timed out (a rank did not arrive)");
+    if (wbad) return fail(LSK_EWEIGHTS, "a weight a_i or b_j is not finite and > 0 (PAPER.md:220)");
     if (brk) return fail(LSK_EBREAKDOWN, "zero or non-finite row dot during Sinkhorn");
+    if (sticky < 0) return sticky;
     if (notconv) {
       g_err = "tolerance not reached within max_iters";
       return LSK_NOT_CONVERGED;
@@ -427,12 +495,10 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
 
 constexpr double kHybridDefault = 0.0;   // set from the measured sweep (DESIGN.md §6 K5)
 
-static size_t solve_ws_bytes(int r, int64_t m, int batch, int gpp_max, int64_t n = 0) {
-  const int64_t rs = r + kExtra + 4;   // partials: r + kExtra + 4 per CTA (column blocks)
-  return 256 * 8 + sizeof(float) * (n + m + 64) * batch +   // implicit row factors h (FACT)
-          sizeof(double) * rs * gpp_max * batch + sizeof(double) * rs * batch +
-         sizeof(double) * kStateDoubles * batch + sizeof(unsigned) * batch +
-         sizeof(float) * m * batch;
+// slot-0 bytes a solve carves besides the caller's own (the implicit row factors h_j of the
+// factored exponent); the solve state lives in slot 1, sized by run_solve after planning
+static size_t solve_ws_bytes(int64_t n, int64_t m, int batch) {
+  return 256 * 8 + (sizeof(float) * (n + m) + 2 * 256) * batch;
 }
 
 static lsk_status check_common(int64_t n, int64_t m, int r, double eps) {
@@ -456,6 +522,28 @@ int64_t lsk_launch_count(int32_t reset) {
   const int64_t v = g_launches;
   if (reset) g_launches = 0;
   return v;
+}
+
+lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
+                          int32_t variant, int32_t* gpp, int32_t* grid) {
+  LSK_TRY(check_common(n, m, r, 1.0));
+  if (!gpp || !grid || batch < 1 || d < 1 || (variant != 1 && variant != 2))
+    return fail(LSK_EINVAL, "bad plan arguments");
+  if (variant == 2 && d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  SinkArgs A{};
+  A.rows[0] = n; A.rows[1] = m;
+  A.r = r; A.d = variant == 2 ? d : 1;
+  static const float dummy = 0.f;   // the factored-exponent instantiation (occupancy only)
+  if (variant == 2) A.hrow[0] = A.hrow[1] = &dummy;
+  SolveCfg c;
+  LSK_TRY(plan_solve(A, variant == 2, batch, nullptr, &c));
+  *gpp = c.gpp;
+  *grid = c.grid;
+  return LSK_OK;
+}
+
+lsk_status lsk_stream_status(void* stream) {
+  return take_sticky(static_cast<cudaStream_t>(stream));
 }
 
 lsk_status lsk_lambert_w0(double z, double* w) {
@@ -543,7 +631,7 @@ static lsk_status feature_map_impl(const lsk_feature_params* p, const float* U, 
   if (!aligned16(Xi)) return fail(LSK_EINVAL, "Xi must be 16-byte aligned");
   char* ws;
   Carve cv;
-  const bool tensor = p->d > 16 && !getenv("LSK_FEATURE_FFMA");   // knob: FFMA A/B only
+  const bool tensor = p->d > 16 && !tuning_env("LSK_FEATURE_FFMA");   // knob: FFMA A/B only
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
   const size_t oD = cv.take(sizeof(float) * p->r);
@@ -655,10 +743,7 @@ lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, 
   A.w[0] = a; A.w[1] = b;
   A.out[0] = u; A.out[1] = v;
   A.r = r; A.d = 1; A.eps = eps;
-  char* ws;
-  LSK_TRY(get_ws(s, solve_ws_bytes(r, m, 1, 2 * num_sms()), &ws));
-  Carve cv;
-  return run_solve(A, false, 1, o, rep, comm, s, ws, cv);
+  return run_solve(A, false, 1, o, rep, comm, s);
 }
 
 // Fraction of each side's rows the hybrid implicit kernel streams (materialised) instead of
@@ -666,7 +751,7 @@ lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, 
 // kernel covers (r <= 1024, d <= 3, one CTA-wide team), bounded by a memory budget.
 static double hybrid_fraction(int r, int d, int64_t n, int64_t m) {
   double phi = kHybridDefault;
-  if (const char* e = getenv("LSK_HYB")) phi = atof(e);
+  if (const char* e = tuning_env("LSK_HYB")) phi = atof(e);
   if (!(phi > 0.0) || r > 1024 || d > 3) return 0.0;
   phi = std::min(phi, 0.9);
   // rows per CTA must leave the recompute team whole tiles to work on
@@ -708,7 +793,7 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   const bool hyb = ns0 + ns1 > 0;
   const size_t oD = hyb ? cv.take(sizeof(float) * p->r) : 0;
   const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r) : 0;
-  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, 1, 2 * num_sms(), n), &ws));
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, 1), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   float* bD = hyb ? reinterpret_cast<float*>(ws + oD) : nullptr;
@@ -743,7 +828,7 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
     A.nstream[0] = ns0;
     A.nstream[1] = ns1;
   }
-  lsk_status st = run_solve(A, true, 1, o, rep, comm, s, ws, cv);
+  lsk_status st = run_solve(A, true, 1, o, rep, comm, s);
   if (stab && rep && st >= 0) {
     double* scratch = reinterpret_cast<double*>(ws + oR);
     LSK_CU(launch_rot_value(u, v, a, b, n, m, 1, scratch + 32, scratch, s, offs, offs + n));
@@ -775,7 +860,7 @@ lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, c
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
-  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(p->r, m, batch, 2 * num_sms(), n), &ws));
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, batch), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
@@ -790,7 +875,7 @@ lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, c
   A.Wt = Wt; A.beta2 = b2;
   A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
   LSK_TRY(setup_fact(A, p->R, batch, s, ws, cv));
-  return run_solve(A, true, batch, o, reps, nullptr, s, ws, cv);
+  return run_solve(A, true, batch, o, reps, nullptr, s);
 }
 
 lsk_status lsk_implicit_row_offsets(const lsk_feature_params* p, const float* U, const float* X,
@@ -830,11 +915,7 @@ lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float
   A.out[0] = u; A.out[1] = v;
   A.wstride[0] = n; A.wstride[1] = m;
   A.r = r; A.d = 1; A.eps = eps;
-  char* ws;
-  LSK_TRY(get_ws(s, solve_ws_bytes(r, m, batch, 64), &ws));
-  Carve cv;
-  if (batch == 1) return run_solve(A, false, 1, o, reps, nullptr, s, ws, cv);
-  return run_solve(A, false, batch, o, reps, nullptr, s, ws, cv);
+  return run_solve(A, false, batch, o, reps, nullptr, s);
 }
 
 lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,
@@ -848,6 +929,7 @@ lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const f
   double* part = reinterpret_cast<double*>(ws + 256);
   double* out2 = reinterpret_cast<double*>(ws);
   LSK_CU(launch_rot_value(u, v, a, b, n, m, 1, part, out2, s));
+  LSK_TRY(take_sticky(s));   // a report-less solve before this read-out broke down
   if (comm) {
     if (!nccl().ok) return fail(LSK_ENCCL, "NCCL not loadable");
     LSK_TRY(nccl_check(nccl().allReduce(out2, out2, 2, ncclFloat64, ncclSum, comm->comm, s),
@@ -905,7 +987,7 @@ static lsk_status divergence_impl(bool impl, const float* F, int64_t n, const fl
     Carve cv2 = cv;   // each solve reuses the same workspace tail
     if (impl) LSK_TRY(setup_fact(A, R, 1, s, ws, cv2));
     lsk_report rep{};
-    lsk_status st = run_solve(A, impl, 1, o, &rep, nullptr, s, ws, cv2);
+    lsk_status st = run_solve(A, impl, 1, o, &rep, nullptr, s);
     if (st < 0) return st;
     if (st > worst) worst = st;
     W[k] = rep.rot;
@@ -996,7 +1078,7 @@ lsk_status lsk_accelerated_sinkhorn(const float* Xi, int64_t n, const float* Zet
       // so the exact block decrease stays >= 0 in floating point), and phi(eta^{k+1})
       const double phi_lam = M1 + M2 + std::log(blk == 1 ? S1 : S2) - la - lb;
       phi_new = std::log(sc[SC_E]) - (blk == 1 ? sc[SC_EW] + lb : la + sc[SC_EW]);
-      if (getenv("LSK_ADEBUG"))   // tuning/debug only
+      if (tuning_env("LSK_ADEBUG"))   // tuning/debug only
         fprintf(stderr, "accel it %d L1 %.3g blk %d n %.3g %.3g phi %.12g -> %.12g\n", it, L1, blk,
                 n1, n2, phi_lam, phi_new);
       // acceptance with an fp64 rounding allowance (reading C29)
@@ -1118,7 +1200,7 @@ lsk_status lsk_sinkhorn_divergence(const float* Xi, int64_t n, const float* Zeta
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t mx = std::max(n, m);
   char* ws;
-  LSK_TRY(get_ws(s, 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(r, mx, 1, 2 * num_sms()), &ws));
+  LSK_TRY(get_ws(s, 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(mx, mx, 1), &ws));
   Carve cv;
   return divergence_impl(false, Xi, n, Zeta, m, r, 1, a, b, eps, nullptr, nullptr, 0.f, 0.0, o,
                          out4_host, reps3, s, ws, cv);
@@ -1139,7 +1221,7 @@ lsk_status lsk_sinkhorn_divergence_implicit(const lsk_feature_params* p, const f
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
-  LSK_TRY(get_ws(s, cv.off + 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(p->r, mx, 1, 2 * num_sms(), mx), &ws));
+  LSK_TRY(get_ws(s, cv.off + 2 * 256 + 2 * sizeof(float) * mx + solve_ws_bytes(mx, mx, 1), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
   LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));

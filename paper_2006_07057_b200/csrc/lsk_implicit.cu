@@ -71,13 +71,14 @@ struct Smem {
   uint64_t full[TEAMS][kRing];     // slot landed (32 cp.async arrivals of the loader warp)
   uint64_t redbar[TEAMS][3];       // row-dot partials of a tile published (TS arrivals)
   float red[TEAMS][3][TR][TS / 32];
-  double xs[2][NWALL];
+  double xs[3][NWALL];
   double xsS[2][SW > 0 ? SW : 1];  // stream warps' error / breakdown sums of a pass
   uint64_t sfull[SW > 0 ? SW : 1][kSRing];   // stream warps' row slots landed (bulk copy tx)
   double ext[kExtra];
   double errL[TEAMS][32];          // per-lane marginal-error sums of the output warps
   double brkL[TEAMS][32];          // per-lane breakdown counts of the output warps
-  double st[3];                    // running solve state: err, breakdowns, final err
+  double wbL[TEAMS][32];           // per-lane bad-weight counts of the output warps
+  double st[4];                    // running solve state: err, breakdowns, final err, bad weights
   int ist[2];                      // final_t, conv
 };
 
@@ -180,17 +181,19 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
   double& stErr = S.st[0];
   double& stBrk = S.st[1];
   double& ferr = S.st[2];
+  double& stWb = S.st[3];
   int& final_t = S.ist[0];
   int& conv = S.ist[1];
   if (tid == 0) {
     stErr = __ldcg(stg_state + ST_ERR);
     stBrk = __ldcg(stg_state + ST_BRK);
+    stWb = __ldcg(stg_state + ST_WBAD);
     ferr = -1.0;
     final_t = -1;
     conv = 0;
   }
   if (tid < 32) {
-    for (int tm = 0; tm < TEAMS; ++tm) S.errL[tm][tid] = S.brkL[tm][tid] = 0.0;
+    for (int tm = 0; tm < TEAMS; ++tm) S.errL[tm][tid] = S.brkL[tm][tid] = S.wbL[tm][tid] = 0.0;
   }
   __syncthreads();
   const int64_t rstride = r + kExtra;
@@ -384,15 +387,18 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       if (tid == 0) {
         const int q = p - 1;
         const int qk = pass_kind(q, A);
-        double e_err, e_brk;
+        double e_err, e_brk, e_wb;
         if (A.gpp > 1) {
           e_err = sv_load(sv_of(A, prob, q) + r, multi);
           e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
+          e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
         } else {
           e_err = S.ext[0];
           e_brk = S.ext[1];
+          e_wb = S.ext[2];
         }
         stBrk += e_brk;
+        stWb += e_wb;
         if (qk == PK_V) {
           const int t = (q + 1) / 2;
           if (t >= 2) {
@@ -571,6 +577,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
             const float w = c * rcp_approx(tj);        // w_j = c_j / t_j
             wt = FACT ? w * h : w;
             if (twarp == NWT - 1 && (lane % G) == 0) {   // outputs: one lane per row
+              if (bad_weight(c)) S.wbL[team][lane] += 1.0;
               if (need_vold) S.errL[team][lane] += fabs((double)sl[64 + row] * (double)tj - (double)c);
               if constexpr (kOut) {
                 if (!(w > 0.f) || !isfinite(w)) S.brkL[team][lane] += 1.0;
@@ -652,27 +659,32 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
     }
 
     // ---------------- end of pass: teams combined (fixed order), cross-CTA fp64 reduction ---
-    double e0 = 0.0, e1 = 0.0;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
     if (!strm && twarp == NWT - 1) {
       e0 = warp_sum_f64(S.errL[team][lane]);
       e1 = warp_sum_f64(S.brkL[team][lane]);
+      e2 = warp_sum_f64(S.wbL[team][lane]);
       S.errL[team][lane] = 0.0;
       S.brkL[team][lane] = 0.0;
+      S.wbL[team][lane] = 0.0;
     }
     if (!strm && twarp == NWT - 1 && lane == 0) {   // hand the team's extras to its thread 0
       S.xs[0][NW - 1 - team] = e0;
       S.xs[1][NW - 1 - team] = e1;
+      S.xs[2][NW - 1 - team] = e2;
     }
     named_bar(1, NT);
     if (!strm && ttid == 0) {
       e0 = S.xs[0][NW - 1 - team];
       e1 = S.xs[1][NW - 1 - team];
+      e2 = S.xs[2][NW - 1 - team];
     }
     named_bar(1, NT);
     if constexpr (TEAMS > 1) {
       if (!strm && team > 0 && ttid == 0) {
         S.xs[0][team] = e0;
         S.xs[1][team] = e1;
+        S.xs[2][team] = e2;
       }
       named_bar(1, NT);
       if (team == 0) {   // fixed order: team 0 + team 1 + ... (deterministic)
@@ -683,6 +695,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
           if (ttid == 0) {
             e0 += S.xs[0][tm];
             e1 += S.xs[1][tm];
+            e2 += S.xs[2][tm];
           }
         }
       }
@@ -720,7 +733,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
                         acc_s[j * 4 + 2][ttid], acc_s[j * 4 + 3][ttid]);
         }
       }
-      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, 0.0, 0.0);
+      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, e2, 0.0);
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[1] = globaltimer();
       // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
@@ -731,6 +744,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       if (tid == 0) {
         S.ext[0] = e0;
         S.ext[1] = e1;
+        S.ext[2] = e2;
       }
       named_bar(1, NT);
     }
@@ -813,12 +827,15 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       stg_state[ST_ERR] = ferr;
       stg_state[ST_CONV] = (double)conv;
       stg_state[ST_BRK] = stBrk;
+      stg_state[ST_WBAD] = stWb;
+      sticky_flags(A, stBrk, stWb);
       __threadfence();
       stg_state[ST_STOP] = 1.0;
     }
   } else if (multi && cta == 0 && tid == 0) {
     stg_state[ST_ERR] = stErr;
     stg_state[ST_BRK] = stBrk;
+    stg_state[ST_WBAD] = stWb;
   }
 }
 
@@ -893,6 +910,7 @@ constexpr size_t dyn_smem() {
 ImplCfg implicit_config(int r, int d) {
   const int r4 = (r + 3) / 4;
   ImplCfg c{};
+#ifdef LSK_TUNING
   {
     // the warp-private kernel is opt-in (LSK_IWARP=1): measured slower than the team kernel on
     // config 2 (26.6 vs 24.0 us per pass, DESIGN.md §6 K5)
@@ -903,15 +921,18 @@ ImplCfg implicit_config(int r, int d) {
       return c;
     }
   }
+#endif
   if (r4 <= 256) c = d <= 3 ? ImplCfg{128, 2, 2, 16, 0, 0} : ImplCfg{128, 4, 2, 4, 0, 0};
   else if (r4 <= 512) c = {512, 1, 1, 8, 0, 0};
   else c = d <= 3 ? ImplCfg{256, 1, 4, 8, 0, 0} : ImplCfg{512, 1, 2, 4, 0, 0};
+#ifdef LSK_TUNING
   if (const char* e = getenv("LSK_ICFG")) {
     ImplCfg x{};
     if (sscanf(e, "%d,%d,%d,%d,%d", &x.ts, &x.teams, &x.nv, &x.tr, &x.pipe) == 5 &&
         x.ts * x.nv * 4 >= r)
       c = x;
   }
+#endif
   return c;
 }
 
@@ -921,15 +942,21 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_D123(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 1) X(TS, TM, NV, TR, P, 2) \
   X(TS, TM, NV, TR, P, 3)
 #define LSK_IMPL_D23(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 2) X(TS, TM, NV, TR, P, 3)
-// defaults (every d; the big-tile ones for d <= 3), then tuning alternatives for d = 2, 3
-#define LSK_IMPL_ALL(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
-  LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                   \
-  LSK_IMPL_D123(X, 256, 1, 4, 8, 0) LSK_IMPL_D23(X, 128, 2, 2, 8, 1)                  \
+// the configurations implicit_config selects (every d; the big-tile ones for d <= 3); tuning
+// builds (-DLSK_TUNING) add the measured alternatives for d = 2, 3 and any LSK_IMPL_EXTRA_H
+#define LSK_IMPL_DEFAULT(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
+  LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                       \
+  LSK_IMPL_D123(X, 256, 1, 4, 8, 0)
+#ifdef LSK_TUNING
+#define LSK_IMPL_ALL(X) LSK_IMPL_DEFAULT(X) LSK_IMPL_D23(X, 128, 2, 2, 8, 1) \
   LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2) LSK_IMPL_EXTRA(X)
-#ifdef LSK_IMPL_EXTRA_H   // tuning builds add instantiations (scripts/build_variant.sh)
+#ifdef LSK_IMPL_EXTRA_H
 #include LSK_IMPL_EXTRA_H
 #else
 #define LSK_IMPL_EXTRA(X)
+#endif
+#else
+#define LSK_IMPL_ALL(X) LSK_IMPL_DEFAULT(X)
 #endif
 
 template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
@@ -960,6 +987,7 @@ static int occupancy_cfg() {
   return nb;
 }
 
+#ifdef LSK_TUNING
 // Hybrid (a.nstream > 0): one 128-thread recompute team (measured 21.7 vs 20.5 us per pass for
 // the two-team default on config 2 — the team's registers are what the stream warps use) plus
 // four stream warps; r <= 1024, d <= 3, plain or factored exponent.
@@ -971,6 +999,7 @@ static cudaError_t launch_hybrid(const SinkArgs& a, bool coop, int grid, cudaStr
 #undef H
   return cudaErrorInvalidConfiguration;
 }
+#endif
 
 // the stabilised mode is instantiated for the default (non-pipelined) configurations only
 template <int TS, int TM, int NV, int TR, int D, int P>
@@ -987,10 +1016,14 @@ static cudaError_t stab_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t
 }
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
-  if (a.nstream[0] + a.nstream[1] > 0) return launch_hybrid(a, coop, grid, s, nullptr);
   const ImplCfg c = implicit_config(a.r, a.d);
+#ifdef LSK_TUNING
+  if (a.nstream[0] + a.nstream[1] > 0) return launch_hybrid(a, coop, grid, s, nullptr);
   if (c.warp && a.stab) return cudaErrorInvalidConfiguration;   // team kernel only
   if (c.warp) return launch_implicit_warp(a, coop, grid, s, nullptr);
+#else
+  if (a.nstream[0] + a.nstream[1] > 0 || c.warp) return cudaErrorInvalidConfiguration;
+#endif
   const int mode = a.stab ? 2 : (a.hrow[0] != nullptr ? 1 : 0);
 #define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
   if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) { \
@@ -1004,15 +1037,19 @@ cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t
 }
 
 int implicit_max_ctas_per_sm(const SinkArgs& a) {
+  const ImplCfg c = implicit_config(a.r, a.d);
+#ifdef LSK_TUNING
   if (a.nstream[0] + a.nstream[1] > 0) {
     int occ = 0;
     return launch_hybrid(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0;
   }
-  const ImplCfg c = implicit_config(a.r, a.d);
   if (c.warp) {
     int occ = 0;
     return launch_implicit_warp(a, false, 0, nullptr, &occ) == cudaSuccess ? occ : 0;
   }
+#else
+  if (a.nstream[0] + a.nstream[1] > 0 || c.warp) return 0;
+#endif
   const int mode = a.stab ? 2 : (a.hrow[0] != nullptr ? 1 : 0);
 #define X(TS_, TM_, NV_, TR_, P_, D_)                                                          \
   if (c.ts == TS_ && c.teams == TM_ && c.nv == NV_ && c.tr == TR_ && c.pipe == P_ && a.d == D_) { \

@@ -10,7 +10,7 @@ namespace lsk {
 constexpr int kConsumerThreads = 256;              // 8 consumer warps per CTA
 constexpr int kThreads = kConsumerThreads + 32;    // + 1 producer warp
 constexpr int kExtra = 4;                          // extras appended to every r-vector:
-                                                   // [0]=err, [1]=breakdown, [2..3]=0
+                                                   // [0]=err, [1]=breakdown, [2]=bad weights, [3]=0
 constexpr int kStateDoubles = 16;                  // per-problem solve state block
 constexpr int kMaxRanks = 8;                       // GPUs of one node in the peer exchange
 // state block layout (doubles)
@@ -23,8 +23,13 @@ enum StateIdx {
   ST_BRK = 8,      // breakdown count
   ST_FINAL_A = 9,  // a^T log u of the returned state
   ST_FINAL_B = 10, // b^T log v of the returned state
-  ST_XERR = 11     // 1 if a cross-GPU peer exchange timed out
+  ST_XERR = 11,    // 1 if a cross-GPU peer exchange timed out
+  ST_WBAD = 12     // count of weights a_i / b_j that are not finite and > 0 (LSK_EWEIGHTS)
 };
+
+// Sticky per-(device, stream) status word (device int, atomicOr'ed by the solve kernels, read
+// and cleared by the synchronising calls: lsk_stream_status, lsk_rot_value, report-taking solves)
+enum StickyBits { STICKY_BREAKDOWN = 1, STICKY_XERR = 2, STICKY_WEIGHTS = 4 };
 
 // Pass schedule: p = 0 init xi-pass (s_v = xi^T 1), p = 2t-1 v-pass of iteration t,
 // p = 2t u-pass of iteration t (t = 1..T), p = 2T+1 error pass (if requested).
@@ -82,6 +87,7 @@ struct SinkArgs {
   int xrs;
   double* xbox[kMaxRanks];
   long long xtimeout_ns;   // a peer poll gives up after this long (ST_XERR, no hang)
+  int* sticky;             // sticky status word of the (device, stream) (StickyBits)
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.

@@ -136,7 +136,10 @@ __device__ __forceinline__ double xrank_total(const SinkArgs& A, int prob, int p
   for (int src = 0; src < N; ++src)
     asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(mine + (int64_t)src * A.xrs), "l"(kSvSentinel)
                  : "memory");
-  if (timed_out) A.state[(int64_t)prob * kStateDoubles + ST_XERR] = 1.0;
+  if (timed_out) {
+    A.state[(int64_t)prob * kStateDoubles + ST_XERR] = 1.0;
+    if (A.sticky) atomicOr(A.sticky, STICKY_XERR);
+  }
   return tot;
 }
 
@@ -225,6 +228,19 @@ __device__ __forceinline__ void r2_cta(const SinkArgs& A, int prob, int pass, co
     r2_block(A, prob, pass, part, cta + A.gpp * m, lane % G2, G2, m < mine);
   }
 }
+
+// end of solve: fold the problem's breakdown / bad-weight counts into the sticky status word
+__device__ __forceinline__ void sticky_flags(const SinkArgs& A, double brk, double wbad) {
+  if (!A.sticky) return;
+  int bits = 0;
+  if (brk > 0.0) bits |= STICKY_BREAKDOWN;
+  if (wbad > 0.0) bits |= STICKY_WEIGHTS;
+  if (bits) atomicOr(A.sticky, bits);
+}
+
+// a Sinkhorn weight (a_i or b_j; mu, nu are probability measures with positive masses,
+// PAPER.md:220) that is not finite and > 0
+__device__ __forceinline__ bool bad_weight(float c) { return !(c > 0.f) || !isfinite(c); }
 
 __device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
   return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];

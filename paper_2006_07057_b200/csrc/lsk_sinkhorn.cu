@@ -48,6 +48,7 @@ struct Smem {
   double ext[kExtra];
   int done_seq;   // last pass finished by the consumers: base(k) + pass, k-th problem of the CTA
   int stop_seq;   // base(k) once the k-th problem of the CTA has stopped (tolerance mode)
+  int mstop;      // multi-launch mode: the consumers stop at the top of this launch
 };
 
 template <int NV, int TR>
@@ -75,6 +76,18 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     for (int i = 0; i < 3; ++i) mbar_init(&S.redbar[i], NT);
     S.done_seq = A.pass_begin - 1;
     S.stop_seq = -1;
+    // Multi-launch mode (one pass per launch, batch 1, gpp >= 2): the consumers' stopping test
+    // on pass pass_begin - 1 runs at the top of the launch, before any tile; decide it here for
+    // the producer too (same inputs, same comparisons), so it never streams a pass the
+    // consumers will not consume (it would block on a full ring).
+    S.mstop = 0;
+    if (A.multi_launch && A.pass_begin > 0) {
+      const int q = A.pass_begin - 1;
+      bool stop = q == A.num_passes - 1;
+      if (A.tol_mode && pass_kind(q, A) == PK_V && (q + 1) / 2 >= 2)
+        stop = stop || __ldcg(sv_of(A, 0, q) + r) < A.tol;
+      S.mstop = stop ? 1 : 0;
+    }
     fence_mbar_init();
   }
   // zero the ring once: tail tiles then compute on finite data without per-row predicates
@@ -85,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 
   // ======================================= producer =======================================
   if (warp == NW) {
+    if (S.mstop) return;
     uint32_t stage = 0, phase = 0;
     const uint64_t pol = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
@@ -173,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   // running solve state (identical in every CTA of the problem)
   double stErr = __ldcg(stg_state + ST_ERR);
   double stBrk = __ldcg(stg_state + ST_BRK);
+  double stWb = __ldcg(stg_state + ST_WBAD);
   double* part = A.part + prob * part_per_problem(r, A.gpp);   // [blk][gpp][4]
   unsigned int nbar = 0;   // group barriers passed for this problem in this launch
   int final_t = -1, conv = 0;
@@ -184,15 +199,18 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     if (have_prev) {
       const int q = p - 1;
       const int qk = pass_kind(q, A);
-      double e_err, e_brk;
+      double e_err, e_brk, e_wb;
       if (A.gpp > 1) {
         e_err = sv_load(sv_of(A, prob, q) + r, multi);
         e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
+        e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
       } else {
         e_err = S.ext[0];
         e_brk = S.ext[1];
+        e_wb = S.ext[2];
       }
       stBrk += e_brk;
+      stWb += e_wb;
       if (qk == PK_V) {
         const int t = (q + 1) / 2;
         if (t >= 2) {
@@ -255,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     if (kind == PK_U) outp = A.out[0] + (int64_t)prob * A.wstride[0];
     if (kind == PK_V) outp = vbuf_ptr(A, prob, (p + 1) / 2);
     const bool err_here = (kind == PK_ERR) || (kind == PK_V && p >= 3);
-    double errsum = 0.0, brksum = 0.0;   // warp 0, lanes < TR
+    double errsum = 0.0, brksum = 0.0, wbsum = 0.0;   // warp 0, lanes < TR
     float4 acc32[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc32[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -288,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
           const float c = st[lane];
           if (kind != PK_ERR) vr_l = __fdiv_rn(c, t);
           if (warp == 0) {
+            if (bad_weight(c)) wbsum += 1.0;
             if (err_here) errsum += fabs((double)st[32 + lane] * (double)t - (double)c);
             if (kind != PK_ERR) {
               if (!(vr_l > 0.f) || !isfinite(vr_l)) brksum += 1.0;
@@ -400,10 +419,11 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     }
 
     // ---------------- end of pass: CTA extras, then cross-CTA fp64 reduction ----------------
-    double e0 = 0.0, e1 = 0.0;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
     if (warp == 0) {
       e0 = warp_sum_f64(errsum);
       e1 = warp_sum_f64(brksum);
+      e2 = warp_sum_f64(wbsum);
     }
     unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
     if (trc) trc[0] = globaltimer();   // tiles done
@@ -413,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       for (int j = 0; j < NV; ++j) {
         if (gv[j]) part_store4(part, A.gpp, g[j], cta, acc64[j][0], acc64[j][1], acc64[j][2], acc64[j][3]);
       }
-      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, 0.0, 0.0);
+      if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, e2, 0.0);
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
       if (trc) trc[1] = globaltimer();   // barrier 1 passed
       // R2: this CTA reduces columns k = cta, cta+gpp, ... in a fixed order
@@ -425,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       if (tid == 0) {
         S.ext[0] = e0;
         S.ext[1] = e1;
+        S.ext[2] = e2;
       }
       named_bar(1, NT);
     }
@@ -490,6 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       stg_state[ST_ERR] = ferr;
       stg_state[ST_CONV] = (double)conv;
       stg_state[ST_BRK] = stBrk;
+      stg_state[ST_WBAD] = stWb;
+      sticky_flags(A, stBrk, stWb);
       __threadfence();
       stg_state[ST_STOP] = 1.0;
     }
@@ -497,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     // multi-launch mode: persist the running state for the next launch
     stg_state[ST_ERR] = stErr;
     stg_state[ST_BRK] = stBrk;
+    stg_state[ST_WBAD] = stWb;
   }
   }   // problems
 }
@@ -515,10 +539,12 @@ void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv) {
   int tt = hi;
   const int budget = std::min(max_stage_bytes, 65536 + kHdr * 4);
   while (tt > lo && (kHdr + tt * r) * 4 > budget) tt >>= 1;
+#ifdef LSK_TUNING
   if (const char* e = getenv("LSK_TR")) {   // tuning knob
     const int x = atoi(e);
     if (x >= lo && x <= hi) tt = x;
   }
+#endif
   *tr = tt;
 }
 

@@ -102,8 +102,9 @@ def test_feature_map_matches_oracle(L, cfg_key, n):
     Xi = torch.empty((n, cfg.r), dtype=torch.float32, device="cuda")
     L.lsk_feature_map(p, U, _dev(prob["X"]), Xi)
     torch.cuda.synchronize()
-    Uo = U.cpu().double().numpy()          # anchor parity is tested separately (<= 1 ulp)
-    ref = O.feature_matrix(prob["X"], Uo, cfg.eps, p.q).T
+    prm = O.gaussian_params(cfg.eps, cfg.d, cfg.r, R)     # the oracle's own a1, a2
+    Uo = O.draw_anchors(cfg.r, cfg.d, prm["sigma"], cfg.anchor_seed)
+    ref = O.feature_matrix(prob["X"], Uo, cfg.eps, prm["q"]).T
     got = Xi.cpu().double().numpy()
     mask = ref > 1e-30
     rel = np.abs(got[mask] - ref[mask]) / ref[mask]
@@ -140,36 +141,28 @@ def test_config2_reduced_ragged(L, variant):
     _check_parity(res, ref)
 
 
-@pytest.mark.parametrize("fact", ["0", "1"])
-@pytest.mark.parametrize("cfg_key,n,m,T,env", [
-    (2, 4099, 3907, 200, {}),                                   # team kernel (128,2,2,16)
-    (2, 4099, 3907, 200, {"LSK_ICFG": "128,4,2,4,0"}),
-    (2, 4099, 3907, 200, {"LSK_ICFG": "128,3,2,8,0"}),
-    (2, 4099, 3907, 200, {"LSK_IWARP": "1"}),                   # warp-private kernel (8,8,1)
-    (2, 4099, 3907, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,8,2"}),
-    (2, 4099, 3907, 200, {"LSK_ICFG": "128,2,2,8,1"}),         # lag-one pipeline
-    (2, 8011, 7993, 200, {"LSK_HYB": "0.3"}),                   # hybrid: 30% of rows streamed
-    (2, 8011, 7993, 200, {"LSK_HYB": "0.6"}),
-    (5, 6151, 6143, 40, {}),                                    # team kernel (256,1,4,8)
-    (5, 6151, 6143, 40, {"LSK_ICFG": "512,1,2,4,0"}),
-    (5, 6151, 6143, 40, {"LSK_ICFG": "256,1,4,2,1"}),
-    (1, 500, 500, 200, {}),
-    (1, 500, 500, 200, {"LSK_IWARP": "1"}),                     # warp-private (16,1,4)
-    (1, 500, 500, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "8,4,4"}),
-    (1, 500, 500, 200, {"LSK_IWARP": "1", "LSK_IWCFG": "16,4,2"})])
-def test_implicit_exponent_forms_and_configs(L, monkeypatch, fact, cfg_key, n, m, T, env):
-    """The implicit kernels' factored exponent (LSK_FACT=1, DESIGN.md §6 K5) and the plain
-    expanded form (LSK_FACT=0), for the default and every instantiated tuning configuration
-    of the warp-private and the team kernel, and the hybrid kernel (LSK_HYB: materialised
-    rows streamed by extra warps of the same launch), against the oracle (ragged n, m: tail
-    tiles)."""
-    monkeypatch.setenv("LSK_FACT", fact)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+@pytest.mark.parametrize("cfg_key,n,m,T,R,eps", [
+    (2, 4099, 3907, 200, 0.0, 0.1),   # team kernel (128,2,2,16), factored exponent (auto R)
+    (2, 4099, 3907, 60, 2.0, 0.09),   # expanded exponent: (log2e/eps) R^2 = 64.1 > 60
+    (5, 6151, 6143, 40, 0.0, 0.05),   # team kernel (256,1,4,8), factored
+    (5, 6151, 6143, 40, 1.6, 0.05),   # expanded: 73.9 > 60
+    (1, 500, 500, 200, 0.0, 0.5),
+    (1, 500, 500, 200, 5.0, 0.5)])    # expanded: 72.1 > 60
+def test_implicit_exponent_forms(L, cfg_key, n, m, T, R, eps):
+    """The implicit kernel's two exponent forms (DESIGN.md §6 K5): the factored one
+    (F = h_j G_jk, used when (log2e/eps) R^2 <= 60) and the plain expanded one (used above it),
+    selected by the data through an explicit R >= max |p| (the map is valid for any such R,
+    PAPER.md:385-391), against the oracle with the same R (ragged n, m: tail tiles).  The
+    tuning-build alternatives (warp-private, hybrid, pipelined) are checked by
+    scripts/tuning_parity.py against the tuning library."""
     cfg = synth.get_config(cfg_key)
+    if R > 0.0:
+        assert 1.4426950408889634 / eps * R * R > 60.0
     prob = synth.make_problem(cfg, n=n, m=m)
-    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
-    res = _run_gpu(L, prob, T, variant="implicit")
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], eps, cfg.r, cfg.anchor_seed, T=T,
+                R=(R if R > 0.0 else None))
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    res = L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, R=R, variant="implicit")
     _check_parity(res, ref)
 
 
@@ -355,8 +348,9 @@ def test_rank_one_full_size_closed_form(L):
     cfg = synth.get_config(5)
     prob = synth.make_problem(cfg, identical_points=True)
     res = _run_gpu(L, prob, 2, variant="implicit")
-    U = res["U"].cpu().double().numpy()
-    q = res["params"]["q"]
+    prm = O.gaussian_params(cfg.eps, cfg.d, cfg.r, O.max_norm(prob["X"], prob["Y"]))
+    U = O.draw_anchors(cfg.r, cfg.d, prm["sigma"], cfg.anchor_seed)   # the oracle's own anchors
+    q = prm["q"]
     xi0 = O.feature_entries_scaled(prob["X"][:1], U, cfg.eps, q, cfg.r, np.zeros(cfg.r, int), np.arange(cfg.r))
     ze0 = O.feature_entries_scaled(prob["Y"][:1], U, cfg.eps, q, cfg.r, np.zeros(cfg.r, int), np.arange(cfg.r))
     kappa = float(xi0 @ ze0)
@@ -566,10 +560,10 @@ def _accel_pair(L, cfg_key, n, m, T):
     L.lsk_feature_map(p, U, _dev(prob["Y"]), Ze)
     gpu = L.lsk_accelerated_sinkhorn(Xi, Ze, _dev(prob["a"]), _dev(prob["b"]), cfg.eps, T,
                                      traces=True)
-    Uo = O.draw_anchors(cfg.r, cfg.d, O.gaussian_params(cfg.eps, cfg.d, cfg.r, R)["sigma"],
-                        cfg.anchor_seed)
-    xi = O.feature_matrix(prob["X"], Uo, cfg.eps, p.q)
-    zeta = O.feature_matrix(prob["Y"], Uo, cfg.eps, p.q)
+    prm = O.gaussian_params(cfg.eps, cfg.d, cfg.r, R)      # the oracle's own a1, a2
+    Uo = O.draw_anchors(cfg.r, cfg.d, prm["sigma"], cfg.anchor_seed)
+    xi = O.feature_matrix(prob["X"], Uo, cfg.eps, prm["q"])
+    zeta = O.feature_matrix(prob["Y"], Uo, cfg.eps, prm["q"])
     ref = O.accelerated_sinkhorn_factored(xi, zeta, prob["a"], prob["b"], cfg.eps, T=T)
     return gpu, ref, (xi, zeta, prob, cfg)
 
@@ -638,7 +632,9 @@ def test_stabilized_feature_map_matches_oracle(L, eps):
     A = torch.empty(n, dtype=torch.float64, device="cuda")
     L.lsk_feature_map_stabilized(p, U, _dev(prob["X"]), Xi, A)
     torch.cuda.synchronize()
-    ref, Aref = O.feature_matrix_stabilized(prob["X"], U.cpu().double().numpy(), eps, p.q)
+    prm = O.gaussian_params(eps, cfg.d, cfg.r, R)
+    ref, Aref = O.feature_matrix_stabilized(
+        prob["X"], O.draw_anchors(cfg.r, cfg.d, prm["sigma"], cfg.anchor_seed), eps, prm["q"])
     got = Xi.cpu().double().numpy()
     assert np.all(got.max(axis=1) == 1.0)                      # every row's largest entry
     mask = ref.T > 1e-30
