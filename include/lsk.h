@@ -333,6 +333,27 @@ lsk_status lsk_comm_destroy(lsk_comm* comm);
  * LSK_P2P=0 in the environment disables the in-kernel exchange.  Synchronises. */
 lsk_status lsk_comm_enable_p2p(lsk_comm* comm, int32_t r_max, void* stream);
 
+/* Emulated ranks (testing and timing the multi-GPU exchange on one GPU): the nranks row
+ * shards of ONE problem (rank q owns rows [q n/N, (q+1) n/N) of X/Xi/a/u and of Y/Zeta/b/v;
+ * n and m divisible by N, 2 <= N <= 8) run as the N problems of one cooperative launch, each
+ * rank a group of CTAs with its own fp64 inbox in this GPU's memory, and the per-half-iteration
+ * all-rank sum of the r-vector (the only datum the shards share) goes through
+ * exactly the in-kernel exchange protocol of lsk_comm_enable_p2p (stores into every rank's
+ * inbox, sentinel polls, rank-order sum, re-arm).  u (n), v (m) are the global scalings; reps
+ * (host, N reports, nullable): rank q's report — every rank computes the same totals, so the
+ * N reports are identical.  Synchronises iff reps != NULL. */
+lsk_status lsk_factored_sinkhorn_emulated(int32_t nranks, const float* Xi, int64_t n,
+                                          const float* Zeta, int64_t m, int32_t r,
+                                          const float* a, const float* b, double eps,
+                                          const lsk_solve_opts* o, float* u, float* v,
+                                          lsk_report* reps, void* stream);
+lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_feature_params* p,
+                                                   const float* U, const float* X, int64_t n,
+                                                   const float* Y, int64_t m, const float* a,
+                                                   const float* b, const lsk_solve_opts* o,
+                                                   float* u, float* v, lsk_report* reps,
+                                                   void* stream);
+
 /* Diagnostic: the launch plan a solve of this shape would use on the current device —
  * gpp = CTAs per problem, grid = CTAs of the launch (grid / gpp = persistent groups; a batched
  * solve with batch > grid / gpp loops each group over several problems).  variant 1 = factor

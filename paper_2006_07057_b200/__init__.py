@@ -72,6 +72,14 @@ _SIGS = {
     "lsk_last_error": (ctypes.c_char_p, []),
     "lsk_launch_count": (c_i64, [c_i32]),
     "lsk_stream_status": (c_i32, [ctypes.c_void_p]),
+    "lsk_factored_sinkhorn_emulated": (c_i32, [c_i32, c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p,
+                                               c_f32p, ctypes.c_double, P(lsk_solve_opts), c_f32p,
+                                               c_f32p, ctypes.c_void_p, ctypes.c_void_p]),
+    "lsk_factored_sinkhorn_implicit_emulated": (c_i32, [c_i32, P(lsk_feature_params), c_f32p,
+                                                        c_f32p, c_i64, c_f32p, c_i64, c_f32p,
+                                                        c_f32p, P(lsk_solve_opts), c_f32p,
+                                                        c_f32p, ctypes.c_void_p,
+                                                        ctypes.c_void_p]),
     "lsk_solve_plan": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, P(c_i32), P(c_i32)]),
     "lsk_lambert_w0": (c_i32, [ctypes.c_double, P(ctypes.c_double)]),
     "lsk_feature_params_init": (c_i32, [ctypes.c_double, c_i32, c_i32, ctypes.c_double,
@@ -335,6 +343,29 @@ def lsk_factored_sinkhorn_implicit_batched(p, U, X, Y, a, b, opts, u, v, report=
         ctypes.byref(p), _f32(U), _f32(X), X.shape[1], _f32(Y), Y.shape[1], B, _f32(a), _f32(b),
         ctypes.byref(opts), _f32(u), _f32(v), reps, _stream(stream)),
         "lsk_factored_sinkhorn_implicit_batched")
+    return list(reps) if report else None
+
+
+def lsk_factored_sinkhorn_emulated(nranks, Xi, Zeta, a, b, eps, opts, u, v, report=True,
+                                   stream=None):
+    """N emulated ranks of one row-sharded streaming solve in one cooperative launch (the
+    in-kernel cross-GPU exchange on one GPU; include/lsk.h).  Returns the N reports."""
+    reps = (lsk_report * nranks)() if report else None
+    _check(_lib.lsk_factored_sinkhorn_emulated(int(nranks), _f32(Xi), Xi.shape[0], _f32(Zeta),
+                                               Zeta.shape[0], Xi.shape[1], _f32(a), _f32(b),
+                                               float(eps), ctypes.byref(opts), _f32(u), _f32(v),
+                                               reps, _stream(stream)),
+           "lsk_factored_sinkhorn_emulated")
+    return list(reps) if report else None
+
+
+def lsk_factored_sinkhorn_implicit_emulated(nranks, p, U, X, Y, a, b, opts, u, v, report=True,
+                                            stream=None):
+    reps = (lsk_report * nranks)() if report else None
+    _check(_lib.lsk_factored_sinkhorn_implicit_emulated(
+        int(nranks), ctypes.byref(p), _f32(U), _f32(X), X.shape[0], _f32(Y), Y.shape[0], _f32(a),
+        _f32(b), ctypes.byref(opts), _f32(u), _f32(v), reps, _stream(stream)),
+        "lsk_factored_sinkhorn_implicit_emulated")
     return list(reps) if report else None
 
 

@@ -368,7 +368,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   SolveCfg c;
   LSK_TRY(plan_solve(A, impl, batch, o, &c));
   if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
-  const bool p2p = comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
+  const bool p2p = !A.emul && comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
                    !(getenv("LSK_P2P") && atoi(getenv("LSK_P2P")) == 0);
   if (comm && c.gpp < 2) {
     // the cross-GPU paths reduce through svec: force >= 2 CTAs
@@ -376,9 +376,23 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     c.grid = c.gpp;
     c.coop = true;
   }
-  A.nranks = 1;
-  A.rank = 0;
-  if (p2p) {   // one persistent launch per GPU; the exchange runs over NVLink inside it
+  if (A.emul) {
+    // emulated ranks (lsk_*_emulated): the batch is the nranks row shards of ONE problem, each
+    // a group of gpp >= 2 CTAs, all co-resident in one cooperative launch (ranks wait on each
+    // other); xbox / nranks / xrs were set by the caller
+    const int slots = num_sms() * std::max(1, impl ? implicit_max_ctas_per_sm(A)
+                                                   : sinkhorn_max_ctas_per_sm(A.nv, A.tr, c.smem));
+    const int64_t rows = std::max(A.rows[0], A.rows[1]);
+    const int want = (int)std::max<int64_t>(2, (rows + 2 * A.tr - 1) / (2 * A.tr));
+    c.gpp = std::max(2, std::min(want, slots / batch));
+    if (c.gpp * batch > slots) return fail(LSK_EUNSUPPORTED, "emulated ranks do not fit on the device");
+    c.grid = c.gpp * batch;
+    c.coop = true;
+  } else {
+    A.nranks = 1;
+    A.rank = 0;
+  }
+  if (p2p && !A.emul) {   // one persistent launch per GPU; the exchange runs over NVLink inside it
     A.nranks = comm->nranks;
     A.rank = comm->rank;
     A.xrs = comm->xrs;
@@ -916,6 +930,88 @@ lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float
   A.wstride[0] = n; A.wstride[1] = m;
   A.r = r; A.d = 1; A.eps = eps;
   return run_solve(A, false, batch, o, reps, nullptr, s);
+}
+
+// ---------------------------------------------------------------- emulated ranks ----------
+// N ranks of one row-sharded solve as the N problems of one cooperative launch on one GPU:
+// rank q owns rows [q n/N, (q+1) n/N) (n, m divisible by N), its own fp64 inbox
+// [2][N][xrs] in this GPU's memory, and runs exactly the in-kernel exchange of
+// lsk_comm_enable_p2p (lsk_sink_common.cuh xrank_total) — the multi-GPU protocol tested and
+// timed where only one GPU exists (B200_PROFILING.md: ranks that wait on one another must not
+// be separate launches on one GPU).
+static lsk_status setup_emulation(SinkArgs& A, int32_t nranks, int64_t n, int64_t m,
+                                  cudaStream_t s) {
+  if (nranks < 2 || nranks > kMaxRanks) return fail(LSK_EINVAL, "nranks must be 2..8");
+  if (n % nranks || m % nranks) return fail(LSK_EINVAL, "n and m must be divisible by nranks");
+  const int xrs = ((A.r + kExtra + 2) + 31) & ~31;
+  char* ws;
+  const size_t per = sizeof(double) * 2 * nranks * xrs;
+  LSK_TRY(get_ws(s, per * nranks, &ws, 2));
+  LSK_CU(cudaMemsetAsync(ws, 0xFF, per * nranks, s));   // all-ones sentinel
+  A.emul = 1;
+  A.nranks = nranks;
+  A.rank = 0;
+  A.xrs = xrs;
+  for (int q = 0; q < nranks; ++q) A.xbox[q] = reinterpret_cast<double*>(ws + per * q);
+  A.xtimeout_ns = 20LL * 1000 * 1000 * 1000;
+  return LSK_OK;
+}
+
+lsk_status lsk_factored_sinkhorn_emulated(int32_t nranks, const float* Xi, int64_t n,
+                                          const float* Zeta, int64_t m, int32_t r,
+                                          const float* a, const float* b, double eps,
+                                          const lsk_solve_opts* o, float* u, float* v,
+                                          lsk_report* reps, void* stream) {
+  LSK_TRY(check_common(n, m, r, eps));
+  if (!Xi || !Zeta || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SinkArgs A{};
+  LSK_TRY(setup_emulation(A, nranks, n, m, s));
+  const int64_t nl = n / nranks, ml = m / nranks;
+  A.F[0] = Xi; A.F[1] = Zeta;
+  A.rows[0] = nl; A.rows[1] = ml;
+  A.fstride[0] = nl * r; A.fstride[1] = ml * r;
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.wstride[0] = nl; A.wstride[1] = ml;
+  A.r = r; A.d = 1; A.eps = eps;
+  return run_solve(A, false, nranks, o, reps, nullptr, s);
+}
+
+lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_feature_params* p,
+                                                   const float* U, const float* X, int64_t n,
+                                                   const float* Y, int64_t m, const float* a,
+                                                   const float* b, const lsk_solve_opts* o,
+                                                   float* u, float* v, lsk_report* reps,
+                                                   void* stream) {
+  if (!p) return fail(LSK_EINVAL, "params NULL");
+  LSK_TRY(check_common(n, m, p->r, p->eps));
+  if (!U || !X || !Y || !a || !b || !u || !v) return fail(LSK_EINVAL, "NULL argument");
+  if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SinkArgs A{};
+  LSK_TRY(setup_emulation(A, nranks, n, m, s));
+  const int64_t nl = n / nranks, ml = m / nranks;
+  char* ws;
+  Carve cv;
+  const size_t oW = cv.take(sizeof(float) * p->d * p->r);
+  const size_t oB = cv.take(sizeof(float) * p->r);
+  LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, 1), &ws));
+  float* Wt = reinterpret_cast<float*>(ws + oW);
+  float* b2 = reinterpret_cast<float*>(ws + oB);
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  A.X[0] = X; A.X[1] = Y;
+  A.rows[0] = nl; A.rows[1] = ml;
+  A.fstride[0] = nl * p->d; A.fstride[1] = ml * p->d;
+  A.w[0] = a; A.w[1] = b;
+  A.out[0] = u; A.out[1] = v;
+  A.wstride[0] = nl; A.wstride[1] = ml;
+  A.r = p->r; A.d = p->d; A.eps = p->eps;
+  A.Wt = Wt; A.beta2 = b2;
+  A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
+  LSK_TRY(setup_fact(A, p->R, nranks, s, ws, cv));
+  return run_solve(A, true, nranks, o, reps, nullptr, s);
 }
 
 lsk_status lsk_rot_value(const float* u, const float* v, const float* a, const float* b,

@@ -88,6 +88,9 @@ struct SinkArgs {
   double* xbox[kMaxRanks];
   long long xtimeout_ns;   // a peer poll gives up after this long (ST_XERR, no hang)
   int* sticky;             // sticky status word of the (device, stream) (StickyBits)
+  int emul;                // 1: the nprob problems of this launch are the nranks ranks of ONE
+                           // row-sharded solve (rank = problem index; xbox[] all on this GPU):
+                           // the cross-GPU exchange emulated inside one cooperative launch
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.

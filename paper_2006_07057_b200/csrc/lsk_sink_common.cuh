@@ -101,17 +101,24 @@ __device__ __forceinline__ double2 sv_load2(const double* p, bool multi) {
 // ---- cross-GPU exchange over NVLink peer memory (one persistent launch per GPU) -----------
 // The owner of column k on every rank (same CTA partition on every rank) adds the ranks' local
 // totals in rank order: it stores its own total into slot [par][my rank][k] of EVERY rank's
-// inbox (st.release.sys through NVLink), polls its own inbox slots [par][src][k] until they
-// differ from the all-ones sentinel (ld.acquire.sys), sums them src = 0, 1, ... (the same bits
-// on every rank: deterministic), and re-arms the slots it consumed.  par alternates with the
-// pass: ranks can be at most one pass apart (pass p+1 needs every rank's pass-p totals), and a
-// slot consumed in pass p is rewritten in pass p+2 only after its source saw this rank's pass
-// p+1 total — which this thread stores after the re-arm (release/acquire causality).  A poll
-// that outlives A.xtimeout_ns sets ST_XERR and yields NaN, so a broken peer cannot hang the GPU.
+// inbox (through NVLink), polls its own inbox slots [par][src][k] until they differ from the
+// all-ones sentinel, sums them src = 0, 1, ... (the same bits on every rank: deterministic),
+// and re-arms the slots it consumed.  par alternates with the pass: ranks can be at most one
+// pass apart (pass p+1 needs every rank's pass-p totals), and a slot consumed in pass p is
+// rewritten (by its source, in pass p+2) only after that source saw this rank's pass p+1
+// total.  Ordering: each value is one aligned 64-bit store (single-copy atomic, so a poll sees
+// the sentinel or the whole value), and ONE fence.acq_rel.sys at the top of each call orders
+// everything this thread did in the previous call — its polls (acquire side: the values it
+// read) and its re-arms (release side) — before the stores of this call; a source's store of
+// pass p+2 therefore follows its poll of this rank's pass-p+1 total, which follows this rank's
+// re-arm of pass p.  (Round 1 used a st.release.sys per store, N fences per call.)  A poll that
+// outlives A.xtimeout_ns sets ST_XERR (and the sticky status) and yields NaN, so a broken
+// peer cannot hang the GPU.  In emulation mode (A.emul) the ranks are the problems of one
+// cooperative launch on one GPU (rank = problem index) — the same code and protocol.
 __device__ __forceinline__ double xpoll(const double* p, long long deadline, int* timed_out) {
   unsigned long long b;
   for (;;) {
-    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
     if (b != kSvSentinel) return __longlong_as_double((long long)b);
     if (*timed_out || (long long)globaltimer() > deadline) {
       *timed_out = 1;
@@ -124,11 +131,13 @@ __device__ __forceinline__ double xpoll(const double* p, long long deadline, int
 __device__ __forceinline__ double xrank_total(const SinkArgs& A, int prob, int par, int k,
                                               double local) {
   const int N = A.nranks;
+  const int me = A.emul ? prob : A.rank;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
   for (int d = 0; d < N; ++d)
-    asm volatile("st.release.sys.global.f64 [%0], %1;" ::"l"(A.xbox[d] + ((int64_t)(par * N + A.rank) * A.xrs + k)),
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(A.xbox[d] + ((int64_t)(par * N + me) * A.xrs + k)),
                  "d"(local)
                  : "memory");
-  double* mine = A.xbox[A.rank] + (int64_t)par * N * A.xrs + k;
+  double* mine = A.xbox[me] + (int64_t)par * N * A.xrs + k;
   const long long deadline = (long long)globaltimer() + A.xtimeout_ns;
   int timed_out = 0;
   double tot = 0.0;
