@@ -356,10 +356,12 @@ lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_fea
 
 /* Diagnostic: the launch plan a solve of this shape would use on the current device —
  * gpp = CTAs per problem, grid = CTAs of the launch (grid / gpp = persistent groups; a batched
- * solve with batch > grid / gpp loops each group over several problems).  variant 1 = factor
- * stream (lsk_factored_sinkhorn[_batched]), 2 = recompute (lsk_factored_sinkhorn_implicit*). */
+ * solve with batch > grid / gpp loops each group over several problems), cluster (nullable) =
+ * 1 if each group is a thread-block cluster whose per-pass r-vector reduction runs over DSMEM
+ * (2 <= gpp <= 8, r <= 1024), 0 if it goes through global memory.  variant 1 = factor stream
+ * (lsk_factored_sinkhorn[_batched]), 2 = recompute (lsk_factored_sinkhorn_implicit*). */
 lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
-                          int32_t variant, int32_t* gpp, int32_t* grid);
+                          int32_t variant, int32_t* gpp, int32_t* grid, int32_t* cluster);
 
 /* Number of kernels the library launched on this thread since the last reset (for the
  * bench's gpu_launches claim). */

@@ -80,7 +80,8 @@ _SIGS = {
                                                         c_f32p, P(lsk_solve_opts), c_f32p,
                                                         c_f32p, ctypes.c_void_p,
                                                         ctypes.c_void_p]),
-    "lsk_solve_plan": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, P(c_i32), P(c_i32)]),
+    "lsk_solve_plan": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, P(c_i32), P(c_i32),
+                               P(c_i32)]),
     "lsk_lambert_w0": (c_i32, [ctypes.c_double, P(ctypes.c_double)]),
     "lsk_feature_params_init": (c_i32, [ctypes.c_double, c_i32, c_i32, ctypes.c_double,
                                         ctypes.c_uint64, c_f32p, c_i64, c_f32p, c_i64,
@@ -185,13 +186,15 @@ def lsk_stream_status(stream=None) -> int:
     return _check(_lib.lsk_stream_status(_stream(stream)), "lsk_stream_status")
 
 
-def lsk_solve_plan(n: int, m: int, r: int, d: int, batch: int = 1, variant: str = "stream"):
-    """(gpp, grid) of the launch a solve of this shape uses (diagnostic; include/lsk.h)."""
-    g, gr = c_i32(), c_i32()
+def lsk_solve_plan(n: int, m: int, r: int, d: int, batch: int = 1, variant: str = "stream",
+                   cluster: bool = False):
+    """(gpp, grid) — and with cluster=True (gpp, grid, cluster) — of the launch a solve of this
+    shape uses (diagnostic; include/lsk.h)."""
+    g, gr, cx = c_i32(), c_i32(), c_i32()
     _check(_lib.lsk_solve_plan(int(n), int(m), int(r), int(d), int(batch),
-                               1 if variant == "stream" else 2, ctypes.byref(g), ctypes.byref(gr)),
-           "lsk_solve_plan")
-    return g.value, gr.value
+                               1 if variant == "stream" else 2, ctypes.byref(g), ctypes.byref(gr),
+                               ctypes.byref(cx)), "lsk_solve_plan")
+    return (g.value, gr.value, cx.value) if cluster else (g.value, gr.value)
 
 
 def launch_count(reset: bool = False) -> int:

@@ -238,7 +238,23 @@ struct SolveCfg {
   bool coop = false;
 };
 
-static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o, SolveCfg* c) {
+// Cluster mode (A.cx, DESIGN.md §6 "pass boundary in a cluster"): a problem's gpp CTAs form one
+// thread-block cluster and the per-pass r-vector reduction runs over DSMEM — for groups of 2..8
+// CTAs (portable cluster sizes) and r <= 1024 (the fp64 partials + totals take 2 x 8 (r+4) B of
+// shared memory).  Not with a communicator or emulated ranks (those reduce through svec).
+constexpr int kCxMaxGpp = 8;
+constexpr int kCxMaxR = 1024;
+static bool cx_size_ok(int gpp, int r) { return gpp >= 2 && gpp <= kCxMaxGpp && r <= kCxMaxR; }
+// a single small problem that would want up to 2 x kCxMaxGpp CTAs runs as one cluster of
+// kCxMaxGpp: each CTA takes up to twice its rows (one more tile per team), the pass boundary
+// drops from ~3 us through global memory to ~1 us over DSMEM
+static int cx_cap(int64_t want, int r, bool allow_cx) {
+  if (!allow_cx || r > kCxMaxR || want < 2 || want > 2 * kCxMaxGpp) return 0;
+  return (int)std::min<int64_t>(want, kCxMaxGpp);
+}
+
+static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o, SolveCfg* c,
+                                bool allow_cx) {
   if (A.r > 4096) return fail(LSK_EDIM, "implicit variant supports r <= 4096");
   const ImplCfg ic = implicit_config(A.r, A.d);
   A.tr = ic.tr;
@@ -252,17 +268,29 @@ static lsk_status plan_implicit(SinkArgs& A, int batch, const lsk_solve_opts* o,
   int occ = implicit_max_ctas_per_sm(A);
   if (occ < 1) return fail(LSK_EUNSUPPORTED, "implicit kernel does not fit on an SM");
   int cps = (o && o->ctas_per_sm > 0) ? std::min(o->ctas_per_sm, occ) : occ;
+  // one tile per team per pass at least: rows / (teams x tr) CTAs
+  const int64_t rows = std::max(A.rows[0], A.rows[1]);
+  const int64_t rpc = (int64_t)ic.teams * tr;
+  const int64_t want = std::max<int64_t>(1, (rows + rpc - 1) / rpc);
+  const int slots = num_sms() * cps;
+  A.cx = 0;
   if (batch > 1) {
+    // one CTA per problem when the batch fills the device; else a cluster of CTAs per problem
     c->gpp = 1;
-    c->grid = batch;
+    const int g = (int)std::min<int64_t>(std::min(kCxMaxGpp, slots / batch), want);
+    if (allow_cx && cx_size_ok(g, A.r)) {
+      c->gpp = g;
+      A.cx = 1;
+    }
+    c->grid = batch * c->gpp;
     c->coop = false;
   } else {
-    const int64_t rows = std::max(A.rows[0], A.rows[1]);
-    const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
-    c->gpp = (int)std::min<int64_t>((int64_t)num_sms() * cps, want);
+    c->gpp = (int)std::min<int64_t>((int64_t)slots, want);
+    if (const int g = cx_cap(want, A.r, allow_cx)) c->gpp = g;
     if (const char* e = tuning_env("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
-    c->coop = c->gpp > 1;
+    A.cx = (allow_cx && cx_size_ok(c->gpp, A.r)) ? 1 : 0;
+    c->coop = c->gpp > 1 && !A.cx;
   }
   return LSK_OK;
 }
@@ -288,8 +316,8 @@ static lsk_status setup_fact(SinkArgs& A, double R, int batch, cudaStream_t s, c
 }
 
 static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_opts* o,
-                             SolveCfg* c) {
-  if (impl) return plan_implicit(A, batch, o, c);
+                             SolveCfg* c, bool allow_cx = true) {
+  if (impl) return plan_implicit(A, batch, o, c, allow_cx);
   c->impl = impl;
   c->batch = batch;
   const int hdr = 64 + 32 * 16;
@@ -297,9 +325,10 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   const size_t static_smem = sinkhorn_static_smem();
   const size_t smem_sm = 227 * 1024;   // B200: 228 KB per SM, 227 KB usable per CTA
   int tr = 0, nv = 0, nst = 0, sf = 0;
+  const size_t cxb = A.r <= kCxMaxR ? cx_part_bytes(A.r) : 0;   // reserved for cluster mode
   for (;; cps = 1) {
     const size_t per_cta =
-        std::min<size_t>(max_smem_optin(), smem_sm / cps - (cps > 1 ? 1024 : 0)) - static_smem - 512;
+        std::min<size_t>(max_smem_optin(), smem_sm / cps - (cps > 1 ? 1024 : 0)) - static_smem - 512 - cxb;
     sinkhorn_tile_config(A.r, (int)(per_cta / 3), &tr, &nv);
     sf = (hdr + tr * A.r + 31) & ~31;
     nst = std::min<int>((int)(per_cta / ((size_t)sf * 4)), 16);
@@ -313,45 +342,61 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   A.nv = nv;
   c->stage_floats = sf;
   c->nstage = nst;
-  c->smem = (size_t)nst * sf * 4;
+  c->smem = (size_t)nst * sf * 4 + cxb;
   int occ = sinkhorn_max_ctas_per_sm(nv, tr, c->smem);
   if (occ < 1) return fail(LSK_EUNSUPPORTED, "sinkhorn kernel does not fit on an SM");
   cps = std::min(cps, occ);
   const int sms = num_sms();
   if (batch > 1) {
     // persistent groups of gpp CTAs, each looping over problems; pick the group size that
-    // keeps the most SMs busy over all rounds, charging gpp > 1 its per-pass group exchange:
-    // t_x ~ 6.4 us against the pass's streaming time at the slot's share of HBM (measured,
-    // config 4, 256 problems: gpp 1 / 2 / 4 / 8 -> 1282 / 1212 / 1312 / 1106 it/s; balance
-    // 86.5% / 86.5% / 98.8% / 92.2%)
+    // keeps the most SMs busy over all rounds, charging gpp > 1 its per-pass group exchange
+    // against the pass's streaming time at the slot's share of HBM: t_x ~ 6.4 us through
+    // global memory (measured round 1, config 4: gpp 1 / 2 / 4 / 8 -> 1282 / 1212 / 1312 /
+    // 1106 it/s), ~1 us as a cluster over DSMEM (2 cluster barriers + DSMEM reads), whose
+    // groups are limited to the clusters that can be resident at once
     const int slots = sms * cps;
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
     const double slot_bw = 6.4e12 / slots;   // bytes/s per CTA slot when all stream
-    int best_g = 1;
+    int best_g = 1, best_ng = std::min(slots, batch);
+    bool best_cx = false;
     double best_eff = -1.0;
     for (int gsz = 1; gsz <= 64 && gsz <= slots; gsz *= 2) {
       if (gsz > 1 && rows / gsz < 2 * tr) break;
-      const int ngroups = slots / gsz;
+      const bool cx = allow_cx && cx_size_ok(gsz, A.r);
+      int ngroups = slots / gsz;
+      if (cx) ngroups = std::min(ngroups, sinkhorn_max_active_clusters(nv, tr, c->smem, gsz));
+      if (ngroups < 1) continue;
       const int rounds = (batch + ngroups - 1) / ngroups;
       const double t_pass = 4.0 * A.r * (double)rows / gsz / slot_bw;
+      const double t_x = cx ? 1.0e-6 : 6.4e-6;
       const double eff = (double)batch * gsz / ((double)rounds * ngroups * gsz) *
                          ((double)ngroups * gsz / slots) *
-                         (gsz == 1 ? 1.0 : t_pass / (t_pass + 6.4e-6));
-      if (eff > best_eff + 1e-9) { best_eff = eff; best_g = gsz; }
+                         (gsz == 1 ? 1.0 : t_pass / (t_pass + t_x));
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        best_g = gsz;
+        best_ng = std::min(ngroups, batch);
+        best_cx = cx;
+      }
     }
-    if (const char* e = tuning_env("LSK_BGPP"))   // tuning knob, clamped to what the grid holds
+    if (const char* e = tuning_env("LSK_BGPP")) {   // tuning knob, clamped to what the grid holds
       best_g = std::max(1, std::min(atoi(e), std::min(64, slots)));
+      best_ng = std::min(slots / best_g, batch);
+      best_cx = false;
+    }
     c->gpp = best_g;
-    const int ngroups = std::min(slots / best_g, batch);
-    c->grid = ngroups * best_g;
-    c->coop = best_g > 1;
+    c->grid = best_ng * best_g;
+    A.cx = best_cx ? 1 : 0;
+    c->coop = best_g > 1 && !best_cx;
   } else {
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
     const int64_t want = std::max<int64_t>(1, (rows + 2 * tr - 1) / (2 * tr));
     c->gpp = (int)std::min<int64_t>((int64_t)sms * cps, want);
+    if (const int g = cx_cap(want, A.r, allow_cx)) c->gpp = g;
     if (const char* e = tuning_env("LSK_GPP")) c->gpp = std::max(1, std::min(c->gpp, atoi(e)));   // tuning knob
     c->grid = c->gpp;
-    c->coop = c->gpp > 1;
+    A.cx = (allow_cx && cx_size_ok(c->gpp, A.r)) ? 1 : 0;
+    c->coop = c->gpp > 1 && !A.cx;
   }
   return LSK_OK;
 }
@@ -366,7 +411,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.want_err = (A.tol_mode || o->want_marginal_err) ? 1 : 0;
   A.num_passes = 2 * A.T + 1 + A.want_err;
   SolveCfg c;
-  LSK_TRY(plan_solve(A, impl, batch, o, &c));
+  LSK_TRY(plan_solve(A, impl, batch, o, &c, !comm && !A.emul));
   if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   const bool p2p = !A.emul && comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
                    !(getenv("LSK_P2P") && atoi(getenv("LSK_P2P")) == 0);
@@ -380,6 +425,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     // emulated ranks (lsk_*_emulated): the batch is the nranks row shards of ONE problem, each
     // a group of gpp >= 2 CTAs, all co-resident in one cooperative launch (ranks wait on each
     // other); xbox / nranks / xrs were set by the caller
+    if (A.r + kExtra + 2 > A.xrs) return fail(LSK_EINVAL, "emulated inboxes too small for r");
     const int slots = num_sms() * std::max(1, impl ? implicit_max_ctas_per_sm(A)
                                                    : sinkhorn_max_ctas_per_sm(A.nv, A.tr, c.smem));
     const int64_t rows = std::max(A.rows[0], A.rows[1]);
@@ -539,7 +585,7 @@ int64_t lsk_launch_count(int32_t reset) {
 }
 
 lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
-                          int32_t variant, int32_t* gpp, int32_t* grid) {
+                          int32_t variant, int32_t* gpp, int32_t* grid, int32_t* cluster) {
   LSK_TRY(check_common(n, m, r, 1.0));
   if (!gpp || !grid || batch < 1 || d < 1 || (variant != 1 && variant != 2))
     return fail(LSK_EINVAL, "bad plan arguments");
@@ -553,6 +599,7 @@ lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t ba
   LSK_TRY(plan_solve(A, variant == 2, batch, nullptr, &c));
   *gpp = c.gpp;
   *grid = c.grid;
+  if (cluster) *cluster = A.cx;
   return LSK_OK;
 }
 
@@ -939,11 +986,12 @@ lsk_status lsk_factored_sinkhorn_batched(const float* Xi, int64_t n, const float
 // lsk_comm_enable_p2p (lsk_sink_common.cuh xrank_total) — the multi-GPU protocol tested and
 // timed where only one GPU exists (B200_PROFILING.md: ranks that wait on one another must not
 // be separate launches on one GPU).
-static lsk_status setup_emulation(SinkArgs& A, int32_t nranks, int64_t n, int64_t m,
+static lsk_status setup_emulation(SinkArgs& A, int32_t nranks, int64_t n, int64_t m, int r,
                                   cudaStream_t s) {
   if (nranks < 2 || nranks > kMaxRanks) return fail(LSK_EINVAL, "nranks must be 2..8");
   if (n % nranks || m % nranks) return fail(LSK_EINVAL, "n and m must be divisible by nranks");
-  const int xrs = ((A.r + kExtra + 2) + 31) & ~31;
+  // every r-vector column (r + kExtra) and the two read-out columns, padded to 32
+  const int xrs = ((r + kExtra + 2) + 31) & ~31;
   char* ws;
   const size_t per = sizeof(double) * 2 * nranks * xrs;
   LSK_TRY(get_ws(s, per * nranks, &ws, 2));
@@ -967,7 +1015,7 @@ lsk_status lsk_factored_sinkhorn_emulated(int32_t nranks, const float* Xi, int64
   if (!aligned16(Xi) || !aligned16(Zeta)) return fail(LSK_EINVAL, "factors must be 16-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SinkArgs A{};
-  LSK_TRY(setup_emulation(A, nranks, n, m, s));
+  LSK_TRY(setup_emulation(A, nranks, n, m, r, s));
   const int64_t nl = n / nranks, ml = m / nranks;
   A.F[0] = Xi; A.F[1] = Zeta;
   A.rows[0] = nl; A.rows[1] = ml;
@@ -991,7 +1039,7 @@ lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_fea
   if (p->d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   SinkArgs A{};
-  LSK_TRY(setup_emulation(A, nranks, n, m, s));
+  LSK_TRY(setup_emulation(A, nranks, n, m, p->r, s));
   const int64_t nl = n / nranks, ml = m / nranks;
   char* ws;
   Carve cv;

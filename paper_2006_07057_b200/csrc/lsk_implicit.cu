@@ -75,6 +75,8 @@ struct Smem {
   double xsS[2][SW > 0 ? SW : 1];  // stream warps' error / breakdown sums of a pass
   uint64_t sfull[SW > 0 ? SW : 1][kSRing];   // stream warps' row slots landed (bulk copy tx)
   double ext[kExtra];
+  double cxext[8];                 // cluster mode: this CTA's extras [0..3], read-out [4..5]
+  uint64_t cxbar;                  // cluster mode: cluster-scope pass barrier
   double errL[TEAMS][32];          // per-lane marginal-error sums of the output warps
   double brkL[TEAMS][32];          // per-lane breakdown counts of the output warps
   double wbL[TEAMS][32];           // per-lane bad-weight counts of the output warps
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
   constexpr int LPR = 32 / TR;                                   // lanes per row after the transpose-reduce
   constexpr int G = exchange_lanes(NWT, LPR);                     // lanes per row in the exchange
   constexpr int PER = NWT / G;                                   // partials summed per lane
-  static_assert(TEAMS >= 1 && TEAMS <= 4, "1 to 4 teams");
+  static_assert(TEAMS >= 1 && TEAMS <= 8, "1 to 8 teams (named barriers 2..9)");
   static_assert(TR * G <= 32 && NWT % G == 0, "exchange layout");
   __shared__ __align__(16) Smem<TS, TEAMS, TR, NW, SW> S;
   // dynamic: fp64 accumulators [NV*4][NT] (element-major: consecutive threads, consecutive
@@ -113,13 +115,15 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
   float4* s_sm = reinterpret_cast<float4*>(slots + TEAMS * kRing * SLOT);   // [NV * TS] s in fp32
   double* sacc0 = reinterpret_cast<double*>(s_sm + NV * TS);   // [SW][GPL * 4][32] stream partials
   float* sring0 = reinterpret_cast<float*>(sacc0 + SW * GPL * 4 * 32);   // [SW][kSRing][kSRow]
+  double* cxtot = reinterpret_cast<double*>(sring0 + SW * kSRing * kSRow);  // cx: [(r/4+1)*4]
+  uint32_t cxphase = 0;
 
   const int tid = threadIdx.x;
   const bool strm = SW > 0 && tid >= NTI;   // a stream warp
   const int team = strm ? TEAMS : tid / TS, ttid = strm ? tid - NTI : tid - team * TS;
   const int warp = tid >> 5, lane = tid & 31;
   const int twarp = ttid >> 5;          // warp index within the team
-  const uint32_t team_bar = 2u + (uint32_t)team;   // named barrier ids 2..5 (1 = whole CTA)
+  const uint32_t team_bar = 2u + (uint32_t)team;   // named barrier ids 2..9 (1 = whole CTA)
   const int prob = blockIdx.x / A.gpp;
   const int cta = blockIdx.x - prob * A.gpp;
   const int r = A.r;
@@ -135,6 +139,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       for (int w = 0; w < SW; ++w)
         for (int i = 0; i < kSRing; ++i) mbar_init(&S.sfull[w][i], 1);
     }
+    if (A.cx) mbar_init(&S.cxbar, (uint32_t)A.gpp);
     fence_mbar_init();
   }
   // zero the slots once: tail rows then compute on finite data without per-row predicates
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
     for (int tm = 0; tm < TEAMS; ++tm) S.errL[tm][tid] = S.brkL[tm][tid] = S.wbL[tm][tid] = 0.0;
   }
   __syncthreads();
+  if (A.cx) cluster_sync_all();   // every CTA's cluster barrier is initialised before any arrive
   const int64_t rstride = r + kExtra;
   double* part = A.part + prob * part_per_problem(r, A.gpp);   // [blk][gpp][4]
   const bool multi = A.multi_launch != 0;
@@ -388,7 +394,13 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         const int q = p - 1;
         const int qk = pass_kind(q, A);
         double e_err, e_brk, e_wb;
-        if (A.gpp > 1) {
+        if (A.cx) {
+          double x[4];
+          cx_total4(cxtot, A.gpp, r >> 2, x);
+          e_err = x[0];
+          e_brk = x[1];
+          e_wb = x[2];
+        } else if (A.gpp > 1) {
           e_err = sv_load(sv_of(A, prob, q) + r, multi);
           e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
           e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
@@ -432,7 +444,11 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       for (int gg = tid; gg < NV * TS; gg += NT) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (gg < R4) {
-          if (A.gpp > 1) {
+          if (A.cx) {
+            double x[4];
+            cx_total4(cxtot, A.gpp, gg, x);
+            v = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+          } else if (A.gpp > 1) {
             const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * gg, multi);
             const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * gg + 2, multi);
             v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
@@ -724,7 +740,22 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
     }
     unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
     if (trc) trc[0] = globaltimer();
-    if (A.gpp > 1) {
+    if (A.cx) {
+      // partials: team 0's acc_s columns (teams already combined) + the extras, in this CTA's
+      // shared memory; owners sum them over DSMEM (lsk_sink_common.cuh cx_*)
+      if (tid == 0) {
+        S.cxext[0] = e0;
+        S.cxext[1] = e1;
+        S.cxext[2] = e2;
+        S.cxext[3] = 0.0;
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+      cx_r2<NT>(A, cxtot, cta, tid, [&](int kb, int q) -> uint32_t {
+        if (kb >= R4) return smem_u32(&S.cxext[q]);
+        return smem_u32(&acc_s[(kb / TS) * 4 + q][kb % TS]);
+      });
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+    } else if (A.gpp > 1) {
       if (team == 0) {
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
@@ -800,7 +831,22 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         lb += S.xs[1][w];
       }
     }
-    if (A.gpp > 1) {
+    if (A.cx) {
+      if (tid == 0) {
+        S.cxext[4] = la;
+        S.cxext[5] = lb;
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+      if (cta == 0 && tid == 0) {
+        la = 0.0;
+        lb = 0.0;
+        for (int c = 0; c < A.gpp; ++c) {
+          la += ld_dsmem_f64(mapa_shared(smem_u32(&S.cxext[4]), (uint32_t)c));
+          lb += ld_dsmem_f64(mapa_shared(smem_u32(&S.cxext[5]), (uint32_t)c));
+        }
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);   // no CTA exits while CTA 0 reads it
+    } else if (A.gpp > 1) {
       if (tid == 0) {
         *part_at(part, A.gpp, (int)rstride, cta) = la;       // columns r+kExtra, r+kExtra+1:
         *part_at(part, A.gpp, (int)rstride + 1, cta) = lb;   // never read by R2 (no race with it)
@@ -901,6 +947,8 @@ constexpr size_t dyn_smem() {
 // (TS, TEAMS, NV, TR, PIPE) per r and d, one CTA per SM.  Larger tiles amortise the per-tile
 // team exchange (measured, DESIGN.md §6 K5); they need the registers of fewer threads.
 // PIPE = 1 holds two feature tiles (lag-one software pipeline).
+//   r <= 128:          eight one-warp teams, 4 columns per thread, 16-row tiles (small r: the
+//                      per-tile exchange stays inside a warp, no padded columns);
 //   r <= 1024, d <= 3: two 128-thread teams, 8 columns per thread, 16-row tiles (255 regs);
 //   r <= 1024, d > 3:  four 128-thread teams, 8 columns per thread, 4-row tiles;
 //   r <= 2048:         one 512-thread team, 4 columns per thread, 8-row tiles;
@@ -922,7 +970,8 @@ ImplCfg implicit_config(int r, int d) {
     }
   }
 #endif
-  if (r4 <= 256) c = d <= 3 ? ImplCfg{128, 2, 2, 16, 0, 0} : ImplCfg{128, 4, 2, 4, 0, 0};
+  if (r4 <= 32) c = ImplCfg{32, 8, 1, 16, 0, 0};   // small r: one warp per team, 8 teams
+  else if (r4 <= 256) c = d <= 3 ? ImplCfg{128, 2, 2, 16, 0, 0} : ImplCfg{128, 4, 2, 4, 0, 0};
   else if (r4 <= 512) c = {512, 1, 1, 8, 0, 0};
   else c = d <= 3 ? ImplCfg{256, 1, 4, 8, 0, 0} : ImplCfg{512, 1, 2, 4, 0, 0};
 #ifdef LSK_TUNING
@@ -944,7 +993,8 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_D23(X, TS, TM, NV, TR, P) X(TS, TM, NV, TR, P, 2) X(TS, TM, NV, TR, P, 3)
 // the configurations implicit_config selects (every d; the big-tile ones for d <= 3); tuning
 // builds (-DLSK_TUNING) add the measured alternatives for d = 2, 3 and any LSK_IMPL_EXTRA_H
-#define LSK_IMPL_DEFAULT(X) LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0) \
+#define LSK_IMPL_DEFAULT(X) LSK_IMPL_D(X, 32, 8, 1, 16, 0)                                 \
+  LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0)                           \
   LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                       \
   LSK_IMPL_D123(X, 256, 1, 4, 8, 0)
 #ifdef LSK_TUNING
@@ -959,14 +1009,33 @@ ImplCfg implicit_config(int r, int d) {
 #define LSK_IMPL_ALL(X) LSK_IMPL_DEFAULT(X)
 #endif
 
+// cluster mode: the owners' fp64 totals follow the dynamic layout
+static size_t cx_smem(const SinkArgs& a) {
+  return a.cx ? sizeof(double) * (size_t)((a.r >> 2) + 1) * 4 : 0;
+}
+
 template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
   auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE, SW>;
-  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>();
+  const size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>() + cx_smem(a);
   constexpr int nthr = TS * TM + 32 * SW;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
-  if (coop) {
+  if (a.cx) {   // one thread-block cluster per problem (gpp CTAs); clusters never wait on each other
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nthr);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.gpp;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  } else if (coop) {
     void* args[] = {(void*)&a};
     e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nthr), args, dyn, s);
   } else {

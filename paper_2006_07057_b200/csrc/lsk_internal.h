@@ -88,6 +88,8 @@ struct SinkArgs {
   double* xbox[kMaxRanks];
   long long xtimeout_ns;   // a peer poll gives up after this long (ST_XERR, no hang)
   int* sticky;             // sticky status word of the (device, stream) (StickyBits)
+  int cx;                  // 1: each problem's gpp CTAs are one thread-block cluster and the
+                           // pass boundary runs over DSMEM (lsk_sink_common.cuh cx_*)
   int emul;                // 1: the nprob problems of this launch are the nranks ranks of ONE
                            // row-sharded solve (rank = problem index; xbox[] all on this GPU):
                            // the cross-GPU exchange emulated inside one cooperative launch
@@ -100,6 +102,10 @@ cudaError_t launch_sinkhorn(const SinkArgs& a, bool cooperative, int grid, size_
 void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv);
 size_t sinkhorn_static_smem();
 int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t dyn_smem);
+// clusters of csize CTAs that can be resident at once (cluster-mode launches)
+int sinkhorn_max_active_clusters(int nv, int tr, size_t dyn_smem, int csize);
+// bytes of dynamic shared memory the cluster mode appends (partials + totals, fp64)
+inline size_t cx_part_bytes(int r) { return 2 * sizeof(double) * (size_t)((r >> 2) + 1) * 4; }
 
 // Implicit (recompute) kernel (lsk_implicit.cu): teams of recompute threads (per-team tile
 // barrier; optional lag-one pipeline), optional stream warps (hybrid, LSK_HYB).

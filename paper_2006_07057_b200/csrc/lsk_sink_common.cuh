@@ -251,6 +251,59 @@ __device__ __forceinline__ void sticky_flags(const SinkArgs& A, double brk, doub
 // PAPER.md:220) that is not finite and > 0
 __device__ __forceinline__ bool bad_weight(float c) { return !(c > 0.f) || !isfinite(c); }
 
+// ---- pass boundary inside a thread-block cluster (A.cx: a problem's gpp <= 8 CTAs are one
+// cluster; small problems) ---------------------------------------------------
+// Each CTA keeps its fp64 partial r-vector (+ extras) in its own shared memory; the owner CTA
+// of column block kb (kb % gpp) sums the gpp partials over DSMEM in CTA order (fixed order:
+// deterministic) into its tot array; every CTA then reads the totals it needs from the owners.
+// Two cluster barriers per pass (partials ready; totals ready) replace the global-memory
+// partials, the atomic group barrier and the svec round trips.
+//
+// cx barrier: consumer thread 0 of every CTA arrives (release, cluster scope) on the mbarrier
+// of every CTA of the cluster (expected count gpp), then waits (acquire) on its own; the named
+// barriers around it order the CTA's other consumer threads (the stream kernel's producer warp
+// never joins: it only talks to its own CTA through the ring).  One mbarrier per CTA is enough:
+// a CTA cannot arrive for instance k+1 on a barrier whose owner has not passed instance k
+// (instance k+1 needs the owner's own arrival, made after its wait on k).
+template <int NTHR>
+__device__ __forceinline__ void cx_barrier(uint64_t* cxbar, uint32_t& cxphase, int G, int tid) {
+  named_bar(1, NTHR);
+  if (tid == 0) {
+    const uint32_t a = smem_u32(cxbar);
+    for (int c = 0; c < G; ++c) mbar_arrive_remote_cluster(mapa_shared(a, (uint32_t)c));
+    while (!mbar_try_wait_cluster(cxbar, cxphase)) {
+    }
+  }
+  cxphase ^= 1u;
+  named_bar(1, NTHR);
+}
+
+// R2 inside the cluster: this CTA (rank cta) sums column blocks kb = cta, cta + G, ...
+// (block r/4: the extras) over the G CTAs' partials; part_addr(kb, q) is the local shared
+// address of element q of block kb of a CTA's partials (the same offset in every CTA).
+// Thread i of the NTHR handles element (i & 3) of the (i >> 2)-th owned block, and so on.
+template <int NTHR, typename PartAddr>
+__device__ __forceinline__ void cx_r2(const SinkArgs& A, double* tot, int cta, int tid,
+                                      PartAddr part_addr) {
+  const int G = A.gpp;
+  const int nblk = (A.r >> 2) + 1;
+  const int mine = (nblk - cta + G - 1) / G;
+  for (int e = tid; e < mine * 4; e += NTHR) {
+    const int kb = cta + G * (e >> 2), q = e & 3;
+    const uint32_t a = part_addr(kb, q);
+    double x = 0.0;
+    for (int c = 0; c < G; ++c) x += ld_dsmem_f64(mapa_shared(a, (uint32_t)c));
+    tot[kb * 4 + q] = x;
+  }
+}
+
+// the four totals of column block kb (its owner's tot array)
+__device__ __forceinline__ void cx_total4(const double* tot, int G, int kb, double (&o)[4]) {
+  const uint32_t a = mapa_shared(smem_u32(tot + kb * 4), (uint32_t)(kb % G));
+  const double2 lo = ld_dsmem_v2f64(a), hi = ld_dsmem_v2f64(a + 16);
+  o[0] = lo.x; o[1] = lo.y; o[2] = hi.x; o[3] = hi.y;
+}
+
 __device__ __forceinline__ float* vbuf_ptr(const SinkArgs& A, int prob, int t) {
   return (((t ^ A.T) & 1) ? A.vbuf1 : A.out[1]) + (int64_t)prob * A.wstride[1];
 }

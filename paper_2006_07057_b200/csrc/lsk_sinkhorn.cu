@@ -46,6 +46,8 @@ struct Smem {
   float red[3][NW][32];
   double xs[2][NW];
   double ext[kExtra];
+  double cxext[2];  // cluster mode: this CTA's read-out partials
+  uint64_t cxbar;   // cluster mode: cluster-scope pass barrier
   int done_seq;   // last pass finished by the consumers: base(k) + pass, k-th problem of the CTA
   int stop_seq;   // base(k) once the k-th problem of the CTA has stopped (tolerance mode)
   int mstop;      // multi-launch mode: the consumers stop at the top of this launch
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         stop = stop || __ldcg(sv_of(A, 0, q) + r) < A.tol;
       S.mstop = stop ? 1 : 0;
     }
+    if (A.cx) mbar_init(&S.cxbar, (uint32_t)A.gpp);
     fence_mbar_init();
   }
   // zero the ring once: tail tiles then compute on finite data without per-row predicates
@@ -95,6 +98,11 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     reinterpret_cast<float4*>(ring)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   fence_proxy_async_smem();
   __syncthreads();
+  if (A.cx) cluster_sync_all();   // all threads (producer too): barriers initialised cluster-wide
+  // cluster mode: this CTA's fp64 partials and the owners' totals, after the ring
+  double* cxpart = reinterpret_cast<double*>(ring + (int64_t)A.nstage * A.stage_floats);
+  double* cxtot = cxpart + ((r >> 2) + 1) * 4;
+  uint32_t cxphase = 0;
 
   // ======================================= producer =======================================
   if (warp == NW) {
@@ -200,7 +208,13 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       const int q = p - 1;
       const int qk = pass_kind(q, A);
       double e_err, e_brk, e_wb;
-      if (A.gpp > 1) {
+      if (A.cx) {
+        double x[4];
+        cx_total4(cxtot, A.gpp, r >> 2, x);
+        e_err = x[0];
+        e_brk = x[1];
+        e_wb = x[2];
+      } else if (A.gpp > 1) {
         e_err = sv_load(sv_of(A, prob, q) + r, multi);
         e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
         e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
@@ -243,7 +257,18 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     if (kind == PK_NONE) continue;
     const int f = (kind == PK_V || kind == PK_ERR) ? 1 : 0;
     if (kind != PK_INIT) {
-      if (A.gpp > 1) {
+      if (A.cx) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          if (gv[j]) {
+            double x[4];
+            cx_total4(cxtot, A.gpp, g[j], x);
+            s[j] = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+          } else {
+            s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      } else if (A.gpp > 1) {
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
@@ -427,7 +452,27 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
     }
     unsigned long long* trc = (A.trace && tid == 0) ? A.trace + ((int64_t)p * A.gpp + cta) * 4 : nullptr;
     if (trc) trc[0] = globaltimer();   // tiles done
-    if (A.gpp > 1) {
+    if (A.cx) {
+      // this CTA's partials to its shared memory; owners sum them over DSMEM
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (gv[j]) {
+          double2* d2 = reinterpret_cast<double2*>(cxpart + 4 * g[j]);
+          d2[0] = make_double2(acc64[j][0], acc64[j][1]);
+          d2[1] = make_double2(acc64[j][2], acc64[j][3]);
+        }
+      }
+      if (tid == 0) {
+        cxpart[4 * (r >> 2) + 0] = e0;
+        cxpart[4 * (r >> 2) + 1] = e1;
+        cxpart[4 * (r >> 2) + 2] = e2;
+        cxpart[4 * (r >> 2) + 3] = 0.0;
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+      cx_r2<NT>(A, cxtot, cta, tid,
+                [&](int kb, int q) -> uint32_t { return smem_u32(cxpart + 4 * kb + q); });
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+    } else if (A.gpp > 1) {
       // R1: block partials part[blk][cta][4] (lsk_sink_common.cuh)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
@@ -484,7 +529,22 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         lb += S.xs[1][w];
       }
     }
-    if (A.gpp > 1) {
+    if (A.cx) {
+      if (tid == 0) {
+        S.cxext[0] = la;
+        S.cxext[1] = lb;
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);
+      if (cta == 0 && tid == 0) {
+        la = 0.0;
+        lb = 0.0;
+        for (int c = 0; c < A.gpp; ++c) {
+          la += ld_dsmem_f64(mapa_shared(smem_u32(&S.cxext[0]), (uint32_t)c));
+          lb += ld_dsmem_f64(mapa_shared(smem_u32(&S.cxext[1]), (uint32_t)c));
+        }
+      }
+      cx_barrier<NT>(&S.cxbar, cxphase, A.gpp, tid);   // no CTA moves on while CTA 0 reads it
+    } else if (A.gpp > 1) {
       if (tid == 0) {
         *part_at(part, A.gpp, (int)rstride, cta) = la;       // columns r+kExtra, r+kExtra+1:
         *part_at(part, A.gpp, (int)rstride + 1, cta) = lb;   // never read by R2 (no race with it)
@@ -557,7 +617,21 @@ static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  if (coop) {
+  if (a.cx) {   // one thread-block cluster per group of gpp CTAs (groups never wait on each other)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.gpp;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  } else if (coop) {
     void* args[] = {(void*)&a};
     e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, s);
   } else {
@@ -586,6 +660,36 @@ cudaError_t launch_sinkhorn(const SinkArgs& a, bool coop, int grid, size_t smem,
   LSK_STREAM_CASES(X)
 #undef X
   return cudaErrorInvalidConfiguration;
+}
+
+template <int NV, int TR>
+static int active_clusters_t(size_t smem, int csize) {
+  auto kern = sinkhorn_kernel<NV, TR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
+}
+
+int sinkhorn_max_active_clusters(int nv, int tr, size_t smem, int csize) {
+#define X(NV_, TR_) if (nv == NV_ && tr == TR_) return active_clusters_t<NV_, TR_>(smem, csize);
+  LSK_STREAM_CASES(X)
+#undef X
+  return 0;
 }
 
 int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t smem) {

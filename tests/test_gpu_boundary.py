@@ -217,3 +217,56 @@ def test_batched_groups_loop_over_problems(L):
         ref = O.rot(bp["X"][q], bp["Y"][q], bp["a"][q], bp["b"][q], cfg.eps, cfg.r,
                     cfg.anchor_seed, T=T, R=R)
         _parity(u[q], v[q], reps[q].rot, ref)
+
+
+# ------------------------------------------------------------- cluster pass boundary --------
+@pytest.mark.parametrize("variant", ["stream", "implicit"])
+@pytest.mark.parametrize("n,m,T", [(500, 500, 200), (1001, 777, 61), (130, 257, 40)])
+def test_cluster_mode_small_problems(L, variant, n, m, T):
+    """Small problems run as one thread-block cluster of 2..8 CTAs whose per-pass r-vector
+    reduction goes over DSMEM (lsk_sink_common.cuh cx_*): the plan says so, and u, v, W_hat
+    match the oracle (config-1 distribution, ragged n != m, both parities of T)."""
+    cfg = synth.get_config(1)
+    gpp, grid, cx = L.lsk_solve_plan(n, m, cfg.r, cfg.d, 1, variant, cluster=True)
+    assert cx == 1 and 2 <= gpp <= 8 and grid == gpp, (gpp, grid, cx)
+    prob = synth.make_problem(cfg, n=n, m=m)
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    res = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T, variant=variant)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
+    _parity(res["u"], res["v"], res["rot"], ref)
+    # tolerance mode: the stop decision from the cluster totals
+    res_t = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, max_iters=500, tol=1e-6,
+                  variant=variant)
+    ref_t = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, tol=1e-6)
+    assert res_t["report"]["converged"] == 1 and abs(res_t["report"]["iters"] - ref_t["iters"]) <= 1
+
+
+def test_cluster_mode_batched(L):
+    """A batch smaller than the device: each problem is a cluster of CTAs (implicit), or groups
+    of cluster CTAs loop over problems (stream)."""
+    import torch
+    cfg = synth.get_config(1)
+    B, n, T = 5, 500, 50
+    for variant in ("stream", "implicit"):
+        gpp, grid, cx = L.lsk_solve_plan(n, n, cfg.r, cfg.d, B, variant, cluster=True)
+        assert cx == 1 and gpp >= 2
+    bp = synth.make_batched(synth.get_config(4, d=2, r=100, eps=0.5), batch=B, n=n, m=n)
+    X, Y, a, b = (_dev(bp[k]) for k in ("X", "Y", "a", "b"))
+    R = max(O.max_norm(bp["X"][q], bp["Y"][q]) for q in range(B))
+    p = L.lsk_feature_params_init(0.5, 2, 100, R, 11)
+    U = torch.empty((100, 2), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    u = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    v = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    reps = L.lsk_factored_sinkhorn_implicit_batched(p, U, X, Y, a, b, L.make_opts(T), u, v)
+    Xi = torch.empty((B, n, 100), dtype=torch.float32, device="cuda")
+    Ze = torch.empty((B, n, 100), dtype=torch.float32, device="cuda")
+    L.lsk_feature_map_batched(p, U, X, Xi)
+    L.lsk_feature_map_batched(p, U, Y, Ze)
+    u2 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    v2 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    reps2 = L.lsk_factored_sinkhorn_batched(Xi, Ze, a, b, 0.5, L.make_opts(T), u2, v2)
+    for q in range(B):
+        ref = O.rot(bp["X"][q], bp["Y"][q], bp["a"][q], bp["b"][q], 0.5, 100, 11, T=T, R=R)
+        _parity(u[q], v[q], reps[q].rot, ref)
+        _parity(u2[q], v2[q], reps2[q].rot, ref)
