@@ -208,15 +208,36 @@ def cpu_baseline(cfg, iters=3):
 
 
 # ======================================================================= lsk arm ==========
-def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1):
+MUFU_PEAK = 4626.0   # Gex2/s measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
+
+
+def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1, stream_rows=(0, 0)):
     """Roofline object of the dominant kernel (the persistent Sinkhorn launch): algorithmic
     bytes (factor stream, HBM-bound) or ex2 (recompute, MUFU-bound) per launch over its mean
-    CUDA-event duration."""
+    CUDA-event duration.  The hybrid (a fraction of the rows streamed, the rest
+    recomputed, both units at once) is bounded by the sum of the two entry rates: MUFU ex2/s +
+    HBM bytes/s / 4 (factor entries/s)."""
     peaks, src = _peaks()
+    ns0, ns1 = stream_rows
+    if var == "implicit" and ns0 + ns1 > 0:
+        entries = float(r) * (n_loc + T * (n_loc + m_loc))
+        streamed = float(r) * (ns0 + T * (ns0 + ns1))
+        achieved = entries / (kmean_ms / 1e3) / 1e9
+        hbm = float(peaks["hbm_gbs"])
+        peak = MUFU_PEAK + hbm / 4.0
+        roof = {"bound": "alu+hbm", "achieved": achieved, "peak": peak, "unit": "Gentries/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "MUFU ex2 measured (profiles/r01_mufu_microbench.txt) + "
+                               "MEASURED_PEAKS.json hbm_gbs (%s) / 4 B per entry" % src,
+                "algorithmic_entries_per_launch": entries,
+                "streamed_fraction": streamed / entries,
+                "mufu_frac_of_recomputed": (entries - streamed) / (kmean_ms / 1e3) / 1e9 / MUFU_PEAK,
+                "hbm_frac_of_streamed": 4.0 * streamed / (kmean_ms / 1e3) / 1e9 / hbm}
+        return roof
     if var == "implicit":
         ex2 = float(r) * (n_loc + T * (n_loc + m_loc)) * batch
         achieved = ex2 / (kmean_ms / 1e3) / 1e9
-        peak = 4626.0   # measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
+        peak = MUFU_PEAK
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gex2/s",
                 "frac": achieved / peak, "traffic": None,
                 "peak_source": "MUFU ex2 measured on B200 (profiles/r01_mufu_microbench.txt)",
@@ -326,7 +347,8 @@ def _timed_loop(C, step, steps, warmup, sample_clocks):
     return tot_ms, kmean, int(launches), clk, res
 
 
-def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True):
+def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True,
+                   stream_fraction=0.0):
     """One problem of config cfg, rows sharded over the ranks: weak scaling (ws x the config's
     rows, each rank holding the config's rows) or strong scaling (the config's rows split).
     value = global iterations/s = T x steps / max-over-ranks device time."""
@@ -342,7 +364,8 @@ def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True):
     U = torch.empty((r, d), dtype=torch.float32, device=C.dev)
     u = torch.empty(n_loc, dtype=torch.float32, device=C.dev)
     v = torch.empty(m_loc, dtype=torch.float32, device=C.dev)
-    opts = L.make_opts(T)
+    opts = L.make_opts(T, stream_fraction=stream_fraction)
+    srows = L.lsk_stream_rows(n_loc, m_loc, r, d, opts) if variant == "implicit" else (0, 0)
     stream = torch.cuda.current_stream()
     Xi = Ze = None
     if variant == "stream":
@@ -371,8 +394,10 @@ def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True):
     tot_ms, kmean, launches, clk, rot = _timed_loop(C, step, steps, warmup, sample_clocks)
     out = {"value": T * steps / (tot_ms / 1e3), "unit": UNIT, "ms_per_step": tot_ms / steps,
            "kernel_ms": kmean, "gpu_launches": launches, "clocks": clk, "rot": rot,
-           "roofline": _roofline(variant, cfg.key, r, n_loc, m_loc, T, kmean),
-           "config": {"workload": "config%d-%s" % (cfg.key, cfg.name), "variant": variant,
+           "roofline": _roofline(variant, cfg.key, r, n_loc, m_loc, T, kmean, stream_rows=srows),
+           "config": {"workload": "config%d-%s" % (cfg.key, cfg.name),
+                      "variant": variant + ("-hybrid" if srows[0] + srows[1] else ""),
+                      "stream_rows": list(srows),
                       "global_n": gn, "global_m": gm, "n_per_gpu": n_loc, "m_per_gpu": m_loc,
                       "d": d, "r": r, "eps": eps, "T": T, "scaling": scaling,
                       "parallelism": "rows%d" % ws if ws > 1 else "single",
@@ -512,11 +537,18 @@ def run_lsk(args):
     # the other variant on the same workload (same protocol), for the comparison the variant
     # choice rests on (d <= 8: both apply)
     if ws == 1 and not args.no_alt and cfg.d <= 8 and cfg.batch == 1:
-        alt = "stream" if variant == "implicit" else "implicit"
-        m = measure_single(C, cfg, alt, args.scaling, args.steps, args.warmup, False)
-        result["alt_variant"] = {"variant": alt, "value": m["value"], "unit": UNIT,
-                                 "ms_per_step": m["ms_per_step"], "kernel_ms": m["kernel_ms"],
-                                 "roofline": m["roofline"], "rot": m["rot"]}
+        alts = []
+        if variant == "implicit" and "hybrid" in result["config"]["variant"]:
+            alts.append(("implicit", -1.0))   # pure recompute (the hybrid's MUFU-only twin)
+        alts.append(("stream" if variant == "implicit" else "implicit", 0.0))
+        result["alt_variants"] = []
+        for alt, sf in alts:
+            m = measure_single(C, cfg, alt, args.scaling, args.steps, args.warmup, False,
+                               stream_fraction=sf)
+            result["alt_variants"].append({"variant": m["config"]["variant"], "value": m["value"],
+                                           "unit": UNIT, "ms_per_step": m["ms_per_step"],
+                                           "kernel_ms": m["kernel_ms"], "roofline": m["roofline"],
+                                           "rot": m["rot"]})
     # end to end through the public host-buffer entry point (N=1)
     if ws == 1 and not args.no_e2e:
         if cfg.batch > 1:

@@ -82,6 +82,13 @@ typedef struct lsk_solve_opts {
   double tol;
   int32_t ctas_per_sm;     /* 0 = library default                                         */
   int32_t flags;           /* LSK_SOLVE_STABILIZE: implicit solver in the row-normalised form */
+  double stream_fraction;  /* implicit solver only: fraction phi of each side's rows whose
+                              factor rows are materialised once and streamed from HBM in every
+                              pass while the rest are regenerated on the MUFU (both units busy
+                              in one launch).  0 = library default (0.25, DESIGN.md §6 K8),
+                              < 0 = off (pure recompute),
+                              in (0, 0.9] = that fraction.  Applies to r <= 1024, d <= 3, large
+                              problems; phi (n + m) r 4 bytes of workspace. */
 } lsk_solve_opts;
 
 /* flags of lsk_solve_opts.  LSK_SOLVE_STABILIZE (lsk_factored_sinkhorn_implicit only; reading
@@ -362,6 +369,12 @@ lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_fea
  * (lsk_factored_sinkhorn[_batched]), 2 = recompute (lsk_factored_sinkhorn_implicit*). */
 lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
                           int32_t variant, int32_t* gpp, int32_t* grid, int32_t* cluster);
+
+/* Diagnostic: the rows of each side (ns0 of X, ns1 of Y) that lsk_factored_sinkhorn_implicit
+ * with these options materialises and streams from HBM (the warp-specialised hybrid kernel);
+ * 0, 0 when it regenerates every row (pure recompute). */
+lsk_status lsk_stream_rows(int64_t n, int64_t m, int32_t r, int32_t d, const lsk_solve_opts* o,
+                           int64_t* ns0, int64_t* ns1);
 
 /* Number of kernels the library launched on this thread since the last reset (for the
  * bench's gpu_launches claim). */

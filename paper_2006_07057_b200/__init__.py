@@ -41,7 +41,7 @@ class lsk_feature_params(ctypes.Structure):
 
 class lsk_solve_opts(ctypes.Structure):
     _fields_ = [("max_iters", c_i32), ("want_marginal_err", c_i32), ("tol", ctypes.c_double),
-                ("ctas_per_sm", c_i32), ("flags", c_i32)]
+                ("ctas_per_sm", c_i32), ("flags", c_i32), ("stream_fraction", ctypes.c_double)]
 
 
 class lsk_report(ctypes.Structure):
@@ -72,6 +72,7 @@ _SIGS = {
     "lsk_last_error": (ctypes.c_char_p, []),
     "lsk_launch_count": (c_i64, [c_i32]),
     "lsk_stream_status": (c_i32, [ctypes.c_void_p]),
+    "lsk_stream_rows": (c_i32, [c_i64, c_i64, c_i32, c_i32, P(lsk_solve_opts), P(c_i64), P(c_i64)]),
     "lsk_factored_sinkhorn_emulated": (c_i32, [c_i32, c_f32p, c_i64, c_f32p, c_i64, c_i32, c_f32p,
                                                c_f32p, ctypes.c_double, P(lsk_solve_opts), c_f32p,
                                                c_f32p, ctypes.c_void_p, ctypes.c_void_p]),
@@ -197,6 +198,15 @@ def lsk_solve_plan(n: int, m: int, r: int, d: int, batch: int = 1, variant: str 
     return (g.value, gr.value, cx.value) if cluster else (g.value, gr.value)
 
 
+def lsk_stream_rows(n: int, m: int, r: int, d: int, opts: lsk_solve_opts = None):
+    """(ns0, ns1): rows of X and Y the implicit solver streams from HBM (hybrid kernel)."""
+    a, b = c_i64(), c_i64()
+    _check(_lib.lsk_stream_rows(int(n), int(m), int(r), int(d),
+                                ctypes.byref(opts) if opts is not None else None,
+                                ctypes.byref(a), ctypes.byref(b)), "lsk_stream_rows")
+    return a.value, b.value
+
+
 def launch_count(reset: bool = False) -> int:
     return int(_lib.lsk_launch_count(1 if reset else 0))
 
@@ -232,9 +242,12 @@ LSK_SOLVE_STABILIZE = 1
 
 
 def make_opts(iters: int, tol: float = 0.0, want_err: bool = False,
-              ctas_per_sm: int = 0, stabilize: bool = False) -> lsk_solve_opts:
+              ctas_per_sm: int = 0, stabilize: bool = False,
+              stream_fraction: float = 0.0) -> lsk_solve_opts:
+    """stream_fraction (implicit solver): 0 = library default, < 0 = pure recompute,
+    (0, 0.9] = that fraction of rows streamed from HBM (include/lsk.h)."""
     return lsk_solve_opts(int(iters), 1 if want_err else 0, float(tol), int(ctas_per_sm),
-                          LSK_SOLVE_STABILIZE if stabilize else 0)
+                          LSK_SOLVE_STABILIZE if stabilize else 0, float(stream_fraction))
 
 
 # ---------------------------------------------------------------- C-ABI mirrors ----------
@@ -547,7 +560,8 @@ def lsk_comm_enable_p2p(comm, r_max: int, stream=None):
 
 # ---------------------------------------------------------------- convenience -----------
 def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
-        want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None, stabilize=False):
+        want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None, stabilize=False,
+        stream_fraction=0.0):
     """Whole hot path on device tensors: a1 params -> a2 anchors -> a3 features -> Alg. 1 ->
     a9 read-out.  variant: "stream" (materialise xi, zeta) or "implicit" (recompute).
     stabilize=True: row-normalised features with log offsets (reading C30; stream: d <= 16,
@@ -563,7 +577,8 @@ def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
     u = torch.empty(n, dtype=torch.float32, device=dev)
     v = torch.empty(m, dtype=torch.float32, device=dev)
     T = iters if iters is not None else (max_iters or 1000)
-    opts = make_opts(T, tol, want_err, ctas_per_sm, stabilize=stabilize and variant == "implicit")
+    opts = make_opts(T, tol, want_err, ctas_per_sm, stabilize=stabilize and variant == "implicit",
+                     stream_fraction=stream_fraction)
     out = dict(params=p.as_dict(), U=U, u=u, v=v)
     if variant == "implicit":
         rep = lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, comm=comm,

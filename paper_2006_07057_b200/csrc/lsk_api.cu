@@ -553,7 +553,13 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   return LSK_OK;
 }
 
-constexpr double kHybridDefault = 0.0;   // set from the measured sweep (DESIGN.md §6 K5)
+// Warp-specialised hybrid (lsk_hybrid.cu) default split: phi = 0.25 of each side's rows
+// streamed, measured on config 2 (us per pass, phi = off / 0.1 / 0.15 / 0.2 / 0.25 / 0.3:
+// 20.44 / 20.84 / 20.49 / 19.35 / 19.13 / 21.84 — past 0.25 the stream team sets the pace;
+// profiles/r02e_hybrid_sweep.log).  The rows beyond whole recompute rounds alone
+// (rows mod 32 SMs, phi 0.053) gained nothing: the recompute teams run ~20% slower per round
+// next to the stream team than alone.
+constexpr double kHybridDefault = 0.25;
 
 // slot-0 bytes a solve carves besides the caller's own (the implicit row factors h_j of the
 // factored exponent); the solve state lives in slot 1, sized by run_solve after planning
@@ -600,6 +606,19 @@ lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t ba
   *gpp = c.gpp;
   *grid = c.grid;
   if (cluster) *cluster = A.cx;
+  return LSK_OK;
+}
+
+static void hybrid_rows(const lsk_solve_opts* o, int r, int d, int64_t n, int64_t m,
+                        int64_t* ns0, int64_t* ns1);
+
+lsk_status lsk_stream_rows(int64_t n, int64_t m, int32_t r, int32_t d, const lsk_solve_opts* o,
+                           int64_t* ns0, int64_t* ns1) {
+  if (!ns0 || !ns1) return fail(LSK_EINVAL, "NULL argument");
+  LSK_TRY(check_common(n, m, r, 1.0));
+  const bool stab = o && (o->flags & LSK_SOLVE_STABILIZE);
+  *ns0 = *ns1 = 0;
+  if (!stab) hybrid_rows(o, r, d, n, m, ns0, ns1);
   return LSK_OK;
 }
 
@@ -807,25 +826,32 @@ lsk_status lsk_factored_sinkhorn(const float* Xi, int64_t n, const float* Zeta, 
   return run_solve(A, false, 1, o, rep, comm, s);
 }
 
-// Fraction of each side's rows the hybrid implicit kernel streams (materialised) instead of
-// regenerating: LSK_HYB=<phi> (0 = off), else the default below for the shapes the hybrid
-// kernel covers (r <= 1024, d <= 3, one CTA-wide team), bounded by a memory budget.
-static double hybrid_fraction(int r, int d, int64_t n, int64_t m) {
-  double phi = kHybridDefault;
+// Fraction of each side's rows the hybrid kernel streams (materialised) instead of regenerating
+// (lsk_solve_opts.stream_fraction: 0 = default, < 0 = off), for the shapes the hybrid kernel
+// covers (r <= 1024, d <= 3; a single problem spread over every SM), bounded by a memory budget.
+static void hybrid_rows(const lsk_solve_opts* o, int r, int d, int64_t n, int64_t m,
+                        int64_t* ns0, int64_t* ns1) {
+  *ns0 = *ns1 = 0;
+  if (r > 1024 || d > 3) return;
+  double phi = (o && o->stream_fraction != 0.0) ? o->stream_fraction : kHybridDefault;
   if (const char* e = tuning_env("LSK_HYB")) phi = atof(e);
-  if (!(phi > 0.0) || r > 1024 || d > 3) return 0.0;
+  if (!(phi > 0.0)) return;   // off
   phi = std::min(phi, 0.9);
-  // rows per CTA must leave the recompute team whole tiles to work on
-  if ((double)std::min(n, m) * (1.0 - phi) < 16.0 * num_sms()) return 0.0;
+  *ns0 = (int64_t)(phi * (double)n);
+  *ns1 = (int64_t)(phi * (double)m);
+  // rows per CTA must leave the recompute teams whole tiles to work on
+  if (std::min(n - *ns0, m - *ns1) < 16 * (int64_t)num_sms()) {
+    *ns0 = *ns1 = 0;
+    return;
+  }
   // at most a quarter of the device memory (queried once: cudaMemGetInfo costs host ms)
   static size_t total = 0;
   if (total == 0) {
     size_t fr = 0;
     if (cudaMemGetInfo(&fr, &total) != cudaSuccess) total = 1;
   }
-  const double bytes = phi * (double)(n + m) * r * 4.0;
-  if (bytes > 0.25 * (double)total) return 0.0;
-  return phi;
+  const double bytes = (double)(*ns0 + *ns1) * r * 4.0;
+  if (bytes > 0.25 * (double)total) *ns0 = *ns1 = 0;
 }
 
 lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const float* U,
@@ -849,8 +875,9 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   const size_t oR = stab ? cv.take(16384) : 0;                      // read-out scratch
   // hybrid: the first phi n (phi m) rows are materialised and streamed by extra warps of the
   // same persistent launch, the rest regenerated (HBM and MUFU busy at once)
-  const double phi = stab ? 0.0 : hybrid_fraction(p->r, p->d, n, m);
-  const int64_t ns0 = (int64_t)(phi * (double)n), ns1 = (int64_t)(phi * (double)m);
+  const bool hyb_ok = !stab && (!comm || comm->p2p);   // not on the NCCL multi-launch path
+  int64_t ns0 = 0, ns1 = 0;
+  if (hyb_ok) hybrid_rows(o, p->r, p->d, n, m, &ns0, &ns1);
   const bool hyb = ns0 + ns1 > 0;
   const size_t oD = hyb ? cv.take(sizeof(float) * p->r) : 0;
   const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r) : 0;

@@ -119,6 +119,10 @@ cudaError_t launch_implicit_warp(const SinkArgs& a, bool cooperative, int grid, 
                                  int* occ);
 cudaError_t launch_implicit(const SinkArgs& a, bool cooperative, int grid, cudaStream_t s);
 int implicit_max_ctas_per_sm(const SinkArgs& a);
+// warp-specialised hybrid (lsk_hybrid.cu): two recompute teams + one stream team per CTA
+bool hybrid_supported(const SinkArgs& a);
+size_t hybrid_smem(int r, int d);
+cudaError_t launch_hybrid_ws(const SinkArgs& a, int grid, cudaStream_t s);
 // stabilised implicit mode: per-row shifts m_j (fp32) and fp64 log offsets A_j (reading C30)
 cudaError_t launch_row_shift(const float* X, int64_t n, int d, const float* Wt,
                              const float* beta2, int r, float c2, float* m2, double* A,

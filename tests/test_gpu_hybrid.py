@@ -1,0 +1,69 @@
+"""The warp-specialised hybrid kernel (lsk_hybrid.cu, DESIGN.md §6 K8): a fraction of each
+side's rows materialised once and streamed from HBM by a third team of every CTA while two
+recompute teams regenerate the rest — against the fp64 oracle (ragged n != m, both exponent
+forms, fixed-T and tolerance mode) and against the pure-recompute solve."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2006_07057_b200 as lib
+    return lib
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _maxrel(gpu, ref):
+    return float(np.max(np.abs(gpu.cpu().double().numpy() - ref) / np.abs(ref)))
+
+
+@pytest.mark.parametrize("phi", [0.0, 0.25, 0.5, 0.8])
+@pytest.mark.parametrize("cfg_key,n,m,T,R,eps", [
+    (2, 8011, 7993, 200, 0.0, 0.1),      # factored exponent
+    (2, 8011, 7993, 61, 2.0, 0.09),      # expanded exponent ((log2e/eps) R^2 > 60)
+    (1, 6000, 5003, 120, 0.0, 0.5),      # small r = 100, d = 2
+])
+def test_hybrid_matches_oracle(L, phi, cfg_key, n, m, T, R, eps):
+    cfg = synth.get_config(cfg_key)
+    opts = L.make_opts(T, stream_fraction=phi)
+    ns = L.lsk_stream_rows(n, m, cfg.r, cfg.d, opts)
+    assert ns[0] > 0 and ns[1] > 0, ns                 # the hybrid path is the one under test
+    prob = synth.make_problem(cfg, n=n, m=m)
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], eps, cfg.r, cfg.anchor_seed, T=T,
+                R=(R if R > 0.0 else None))
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    res = L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, R=R, variant="implicit",
+                stream_fraction=phi)
+    assert abs(res["rot"] - ref["rot"]) <= 1e-5 * abs(ref["rot"])
+    assert _maxrel(res["u"], ref["u"]) <= 1e-4 and _maxrel(res["v"], ref["v"]) <= 1e-4
+    pure = L.rot(X, Y, a, b, eps, cfg.r, cfg.anchor_seed, iters=T, R=R, variant="implicit",
+                 stream_fraction=-1.0)
+    assert abs(res["rot"] - pure["rot"]) <= 1e-6 * abs(pure["rot"])
+
+
+def test_hybrid_tolerance_and_determinism(L):
+    import torch
+    cfg = synth.get_config(2)
+    prob = synth.make_problem(cfg, n=10000, m=9999)
+    X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
+    tol = 1e-5
+    r1 = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, max_iters=400, tol=tol,
+               variant="implicit", stream_fraction=0.3)
+    r2 = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, max_iters=400, tol=tol,
+               variant="implicit", stream_fraction=0.3)
+    assert r1["report"]["converged"] == 1 and r1["report"]["marginal_err"] < tol
+    assert torch.equal(r1["u"], r2["u"]) and torch.equal(r1["v"], r2["v"]) and r1["rot"] == r2["rot"]
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, tol=tol)
+    assert abs(r1["report"]["iters"] - ref["iters"]) <= 1
