@@ -29,7 +29,7 @@ def _maxrel(gpu, ref):
     return float(np.max(np.abs(gpu.cpu().double().numpy() - ref) / np.abs(ref)))
 
 
-@pytest.mark.parametrize("phi", [0.0, 0.25, 0.5, 0.8])
+@pytest.mark.parametrize("phi", [0.0, 0.25, 0.5])
 @pytest.mark.parametrize("cfg_key,n,m,T,R,eps", [
     (2, 8011, 7993, 200, 0.0, 0.1),      # factored exponent
     (2, 8011, 7993, 61, 2.0, 0.09),      # expanded exponent ((log2e/eps) R^2 > 60)
