@@ -873,14 +873,27 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   const size_t oM = stab ? cv.take(sizeof(float) * (n + m)) : 0;    // row shifts m_j
   const size_t oA = stab ? cv.take(sizeof(double) * (n + m)) : 0;   // row offsets A_j
   const size_t oR = stab ? cv.take(16384) : 0;                      // read-out scratch
+  // tensor-core exponent kernel (lsk_implicit_tc.cu, DESIGN.md §6 K9): measured slower than
+  // the FFMA-exponent kernel, so only tuning builds select it (LSK_ITC=1; r <= 1024, d <= 2,
+  // factored exponent, not on the NCCL multi-launch path, no streamed fraction)
+#ifdef LSK_TUNING
+  const char* itc_env = tuning_env("LSK_ITC");
+  const bool tc_ok = itc_env && atoi(itc_env) == 1 && !stab && p->d <= 2 && p->r <= 1024 &&
+                     (!comm || comm->p2p) && !(o && o->stream_fraction > 0.0);
+#else
+  const bool tc_ok = false;
+#endif
   // hybrid: the first phi n (phi m) rows are materialised and streamed by extra warps of the
   // same persistent launch, the rest regenerated (HBM and MUFU busy at once)
-  const bool hyb_ok = !stab && (!comm || comm->p2p);   // not on the NCCL multi-launch path
+  const bool hyb_ok = !stab && !tc_ok && (!comm || comm->p2p);   // not on the NCCL multi-launch path
   int64_t ns0 = 0, ns1 = 0;
   if (hyb_ok) hybrid_rows(o, p->r, p->d, n, m, &ns0, &ns1);
   const bool hyb = ns0 + ns1 > 0;
   const size_t oD = hyb ? cv.take(sizeof(float) * p->r) : 0;
   const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r) : 0;
+#ifdef LSK_TUNING
+  const size_t oI = tc_ok ? cv.take(sizeof(float) * itc_image_floats(n + m)) : 0;
+#endif
   LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, 1), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
@@ -906,6 +919,15 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   } else {
     LSK_TRY(setup_fact(A, p->R, 1, s, ws, cv));
   }
+#ifdef LSK_TUNING
+  if (tc_ok && A.hrow[0] != nullptr) {   // the B images of both sides (packed 3xTF32 rows)
+    float* img = reinterpret_cast<float*>(ws + oI);
+    LSK_CU(launch_itc_image(X, n, p->d, img, s));
+    LSK_CU(launch_itc_image(Y, m, p->d, img + itc_image_floats(n), s));
+    A.bimg[0] = img;
+    A.bimg[1] = img + itc_image_floats(n);
+  }
+#endif
   if (hyb) {
     float* F0 = reinterpret_cast<float*>(ws + oF);
     float* F1 = F0 + ns0 * p->r;

@@ -1086,6 +1086,9 @@ static cudaError_t stab_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t
 
 cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
   const ImplCfg c = implicit_config(a.r, a.d);
+#ifdef LSK_TUNING
+  if (itc_supported(a)) return launch_itc(a, grid, s);
+#endif
   if (a.nstream[0] + a.nstream[1] > 0 && hybrid_supported(a)) return launch_hybrid_ws(a, grid, s);
 #ifdef LSK_TUNING
   if (a.nstream[0] + a.nstream[1] > 0) return launch_hybrid(a, coop, grid, s, nullptr);
@@ -1108,6 +1111,7 @@ cudaError_t launch_implicit(const SinkArgs& a, bool coop, int grid, cudaStream_t
 
 int implicit_max_ctas_per_sm(const SinkArgs& a) {
   const ImplCfg c = implicit_config(a.r, a.d);
+  if (a.bimg[0] != nullptr) return 1;   // tensor-core exponent kernel (all of TMEM per CTA)
   if (a.nstream[0] + a.nstream[1] > 0 && a.r <= 1024 && a.d <= 3 && !a.stab) return 1;   // hybrid
 #ifdef LSK_TUNING
   if (a.nstream[0] + a.nstream[1] > 0) {

@@ -90,6 +90,9 @@ struct SinkArgs {
   int* sticky;             // sticky status word of the (device, stream) (StickyBits)
   int cx;                  // 1: each problem's gpp CTAs are one thread-block cluster and the
                            // pass boundary runs over DSMEM (lsk_sink_common.cuh cx_*)
+  // tensor-core exponent kernel (lsk_implicit_tc.cu): per side the packed 3xTF32 B image of
+  // the point rows, 8 floats per row ([ph | ph | pl | 1 1 | 0 ..]); NULL = not used
+  const float* bimg[2];
   int emul;                // 1: the nprob problems of this launch are the nranks ranks of ONE
                            // row-sharded solve (rank = problem index; xbox[] all on this GPU):
                            // the cross-GPU exchange emulated inside one cooperative launch
@@ -123,6 +126,12 @@ int implicit_max_ctas_per_sm(const SinkArgs& a);
 bool hybrid_supported(const SinkArgs& a);
 size_t hybrid_smem(int r, int d);
 cudaError_t launch_hybrid_ws(const SinkArgs& a, int grid, cudaStream_t s);
+// tensor-core exponent kernel (lsk_implicit_tc.cu): r <= 1024, d <= 2, factored exponent,
+// one problem over >= 2 CTAs (no cluster / multi-launch / emulation / hybrid)
+bool itc_supported(const SinkArgs& a);
+size_t itc_image_floats(int64_t rows);
+cudaError_t launch_itc_image(const float* X, int64_t n, int d, float* img, cudaStream_t s);
+cudaError_t launch_itc(const SinkArgs& a, int grid, cudaStream_t s);
 // stabilised implicit mode: per-row shifts m_j (fp32) and fp64 log offsets A_j (reading C30)
 cudaError_t launch_row_shift(const float* X, int64_t n, int d, const float* Wt,
                              const float* beta2, int r, float c2, float* m2, double* A,
