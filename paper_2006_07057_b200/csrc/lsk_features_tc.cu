@@ -15,6 +15,7 @@
 // chunk; tcgen05.commit signals an mbarrier that releases the buffers and, after the last
 // chunk, the epilogue: 8 warps read the accumulator with tcgen05.ld (warp w: TMEM lanes
 // 32(w%4).., columns 128(w/4)..), add alpha2 + beta2, MUFU ex2, store fp32.
+#include <algorithm>
 #include <cmath>
 
 #include "lsk_internal.h"
@@ -268,9 +269,362 @@ __global__ void __launch_bounds__(kThreads, 2) feature_map_tc_kernel(
 
 }  // namespace tc
 
+// ============================================================================================
+// Persistent, warp-specialised version (round 2; d <= 128): the CTA keeps ONE 128-anchor block
+// of the W hi/lo images resident in shared memory (the A operand, loaded once) and streams
+// 128-row tiles of X through a 2-slot ring (the B operand):
+//   warps 0-3  (loaders)  X chunk (128 rows x 32 k) -> hi/lo split -> SW128 images, |x|^2;
+//   warp 4..7  (epilogue) TMEM accumulator -> 2^(alpha_i + beta2_k + G) (or the arc-cosine
+//                          form) -> fp32 stores, one per register across the 32 lanes = 128
+//                          contiguous bytes of a row (the anchors are the MMA's M, on the TMEM
+//                          lanes; the rows are its N, on the columns);
+//   warp 8     (MMA)      one elected thread: 3 x 4 tcgen05.mma (128 x 128 x 8) per chunk into a
+//                          double-buffered TMEM accumulator; tcgen05.commit frees the X slot
+//                          and, after the last chunk, hands the buffer to the epilogue.
+// CTA c serves anchor block c % NTN and row tiles c / NTN, c / NTN + G, ... (G = grid / NTN):
+// the NTN CTAs of a row tile run side by side, so X comes from HBM once and from L2 after.
+namespace tc2 {
+using tc::swz128;
+using tc::tf32_rna;
+using tc::umma_desc_sw128;
+using tc::mma_tf32;
+using tc::mma_commit;
+using tc::tc_fence_after;
+using tc::tc_fence_before;
+
+
+constexpr int BM = 128;             // anchors per CTA (MMA M)
+constexpr int BNR = 128;            // rows per tile (MMA N)
+constexpr int BK = 32;              // k per chunk (one 128-byte swizzle row)
+constexpr int kMaxChunks = 4;       // d <= 128
+constexpr int kSlots = 2;
+constexpr int kImg = 128 * 128;     // bytes of one 128-row x 32-k tf32 image (16 KB)
+constexpr int kThreads = 288;       // 4 loader warps, 4 epilogue warps, 1 MMA warp
+constexpr int kAlphaRing = 4;
+// smem: W images [nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | barriers
+constexpr int kOffW = 0;
+constexpr int kOffX = kOffW + kMaxChunks * 2 * kImg;
+constexpr int kOffAlpha = kOffX + kSlots * 2 * kImg;
+constexpr int kOffBar = kOffAlpha + kAlphaRing * BNR * 4;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;   // + alignment slack
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BNR >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+// W hi/lo images for 128-anchor blocks: [nt][kc][2][128 rows x 128 B swizzled]
+__global__ void w_images_kernel(const float* __restrict__ U, int r, int d, double sc,
+                                float* __restrict__ img) {
+  const int nt = blockIdx.x, kc = blockIdx.y;
+  const int nkc = gridDim.y;
+  char* base = reinterpret_cast<char*>(img) + ((size_t)nt * nkc + kc) * 2 * kImg;
+  for (int i = threadIdx.x; i < BM * BK; i += blockDim.x) {
+    const int row = i / BK, k = i % BK;
+    const int n = nt * BM + row, c = kc * BK + k;
+    const float w = (n < r && c < d) ? (float)(sc * (double)U[(int64_t)n * d + c]) : 0.f;
+    const float hi = tf32_rna(w);
+    const float lo = tf32_rna(w - hi);
+    *reinterpret_cast<float*>(base + swz128(row, k)) = hi;
+    *reinterpret_cast<float*>(base + kImg + swz128(row, k)) = lo;
+  }
+}
+
+template <int MODE>   // 0: Gaussian 2^(alpha + beta2 + G); 1: arc-cosine beta2 relu(G)^sdeg
+__global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
+    const float* __restrict__ X, int64_t M, int d, const float* __restrict__ wimg,
+    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int sdeg) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* wbar = bars;                  // W images landed
+  uint64_t* xfull = bars + 1;             // [kSlots] X chunk written (128 loader arrivals)
+  uint64_t* xempty = bars + 1 + kSlots;   // [kSlots] X chunk consumed (tcgen05.commit)
+  uint64_t* tfull = bars + 1 + 2 * kSlots;       // [2] accumulator ready (tcgen05.commit)
+  uint64_t* tempty = bars + 3 + 2 * kSlots;      // [2] accumulator drained (128 epilogue arrivals)
+  uint64_t* abar = bars + 5 + 2 * kSlots;        // [kAlphaRing] alpha of a tile written (128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * kSlots + kAlphaRing);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntn = (r + BM - 1) / BM;
+  const int groups = gridDim.x / ntn;
+  const int nt = blockIdx.x % ntn, grp = blockIdx.x / ntn;
+  const int nkc = (d + BK - 1) / BK;
+  const int64_t mtiles = (M + BNR - 1) / BNR;
+  const int n0 = nt * BM;
+
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(2 * BNR)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(xfull + i, 128);
+      mbar_init(xempty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, 128);
+    }
+    for (int i = 0; i < kAlphaRing; ++i) mbar_init(abar + i, 128);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (warp < 4) {
+    // ------------------------------ loaders ---------------------------------------------
+    if (tid == 0) {   // this CTA's anchor block of the W images, once
+      const uint32_t bytes = (uint32_t)nkc * 2u * kImg;
+      mbar_arrive_expect_tx(wbar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              sbase + kOffW),
+          "l"(reinterpret_cast<const char*>(wimg) + (size_t)nt * nkc * 2 * kImg), "r"(bytes),
+          "r"(smem_u32(wbar))
+          : "memory");
+    }
+    // thread t: 16-byte k-quad q = t % 8 of rows t / 8 + 16 j (j = 0..7) of the chunk
+    const int q = tid & 7, rb = tid >> 3;
+    const bool vec = (d & 3) == 0;
+    // the chunks of this CTA's tiles as one sequence; the next chunk's global loads are in
+    // flight (registers) while the current one is split and stored
+    auto load_chunk = [&](int64_t mt, int kc, float4 (&v)[8]) {
+      const int64_t m0 = mt * BNR;
+      const int c0 = kc * BK + 4 * q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t row = m0 + rb + 16 * j;
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < M) {
+          const float* src = X + row * d + c0;
+          if (vec && c0 + 4 <= d) {
+            v[j] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            float* e = &v[j].x;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] = (c0 + u < d) ? __ldg(src + u) : 0.f;
+          }
+        }
+      }
+    };
+    uint32_t it = 0;   // chunks so far (slot it % kSlots)
+    int ti = 0;        // tiles so far (alpha ring)
+    int64_t mt = grp;
+    int kc = 0;
+    float xx[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // a 3-deep register queue: chunks it+1 and it+2 are in flight while chunk it is split
+    float4 cur[8], n1[8], n2[8];
+    auto advance = [&](int64_t& m, int& c) {
+      if (++c == nkc) {
+        c = 0;
+        m += groups;
+      }
+    };
+    int64_t m1 = mt, m2;
+    int k1 = kc, k2;
+    if (mt < mtiles) load_chunk(mt, 0, cur);
+    advance(m1, k1);
+    if (m1 < mtiles) load_chunk(m1, k1, n1);
+    m2 = m1;
+    k2 = k1;
+    advance(m2, k2);
+    while (mt < mtiles) {
+      if (m2 < mtiles) load_chunk(m2, k2, n2);
+      const int slot = (int)(it % kSlots);
+      if (it >= (uint32_t)kSlots) mbar_wait(xempty + slot, ((it / kSlots) - 1) & 1u);
+      unsigned char* xs = smem + kOffX + slot * 2 * kImg;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 hi, lo;
+        const float* e = &cur[j].x;
+        float* h = &hi.x;
+        float* l = &lo.x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          xx[j] = fmaf(e[u], e[u], xx[j]);
+          h[u] = tf32_rna(e[u]);
+          l[u] = tf32_rna(e[u] - h[u]);
+        }
+        const uint32_t off = swz128(rb + 16 * j, 4 * q);
+        *reinterpret_cast<float4*>(xs + off) = hi;
+        *reinterpret_cast<float4*>(xs + kImg + off) = lo;
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(xfull + slot);
+      ++it;
+      if (kc == nkc - 1) {
+        // alpha_i = c2 |x_i|^2: the 8 k-quads of a row are 8 consecutive lanes
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float t = xx[j];
+          t += __shfl_xor_sync(0xffffffffu, t, 1);
+          t += __shfl_xor_sync(0xffffffffu, t, 2);
+          t += __shfl_xor_sync(0xffffffffu, t, 4);
+          if (q == 0) alpha_s[(ti % kAlphaRing) * BNR + rb + 16 * j] = c2 * t;
+          xx[j] = 0.f;
+        }
+        // ring entry ti % 4 is rewritten at tile ti + 4, after the MMAs of tile ti + 3, which
+        // follow the epilogue's release of tile ti + 1's accumulator: alpha(ti) was read by then
+        mbar_arrive(abar + (ti % kAlphaRing));
+        ++ti;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cur[j] = n1[j];
+        n1[j] = n2[j];
+      }
+      mt = m1;
+      kc = k1;
+      m1 = m2;
+      k1 = k2;
+      advance(m2, k2);
+    }
+  } else if (warp < 8) {
+    // ------------------------------ epilogue --------------------------------------------
+    const int qd = warp & 3;                    // TMEM lane quarter = anchors 32 qd ..
+    const int k = n0 + 32 * qd + lane;          // this thread's anchor
+    const bool kv = k < r;
+    const float bk = kv ? beta2[k] : 0.f;
+    int ti = 0;
+    for (int64_t mt = grp; mt < mtiles; mt += groups, ++ti) {
+      const int64_t m0 = mt * BNR;
+      const int buf = ti & 1;
+      mbar_wait(abar + (ti % kAlphaRing), (uint32_t)(ti / kAlphaRing) & 1u);   // alpha written
+      mbar_wait(tfull + buf, (uint32_t)(ti >> 1) & 1u);
+      tc_fence_after();
+      const float* al = alpha_s + (ti % kAlphaRing) * BNR;
+#pragma unroll 1
+      for (int g = 0; g < BNR / 32; ++g) {
+        uint32_t a[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(buf * BNR + 32 * g);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+              "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]),
+              "=r"(a[13]), "=r"(a[14]), "=r"(a[15]), "=r"(a[16]), "=r"(a[17]), "=r"(a[18]),
+              "=r"(a[19]), "=r"(a[20]), "=r"(a[21]), "=r"(a[22]), "=r"(a[23]), "=r"(a[24]),
+              "=r"(a[25]), "=r"(a[26]), "=r"(a[27]), "=r"(a[28]), "=r"(a[29]), "=r"(a[30]),
+              "=r"(a[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (g == BNR / 32 - 1) {   // the buffer is drained: the next tile's MMAs may start
+          tc_fence_before();
+          mbar_arrive(tempty + buf);
+        }
+        const int64_t rg = m0 + 32 * g;
+        if (kv) {
+          // one 64-bit base per 32-row group; rows as 32-bit offsets (32 ld < 2^31); a lane's
+          // store j and its neighbours' form 128 contiguous bytes of row rg + j
+          float* dst = Xi + rg * ld + k;
+          const int nrow = (M - rg) < 32 ? (int)(M - rg) : 32;
+          float o[32];
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 a4 = *reinterpret_cast<const float4*>(al + 32 * g + j);
+            const float* ap = &a4.x;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float acc = __uint_as_float(a[j + u]);
+              if (MODE == 0) {
+                o[j + u] = ex2((ap[u] + bk) + acc);
+              } else {
+                const float rl = fmaxf(acc, 0.f);
+                o[j + u] = bk * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
+              }
+            }
+          }
+          if (nrow == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcs(dst + j * ld, o[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nrow) __stcs(dst + j * ld, o[j]);
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------ MMA issuer ------------------------------------------
+    if (lane == 0) {
+      mbar_wait(wbar, 0);
+      uint32_t it = 0;
+      int ti = 0;
+      for (int64_t mt = grp; mt < mtiles; mt += groups, ++ti) {
+        const int buf = ti & 1;
+        if (ti >= 2) mbar_wait(tempty + buf, (uint32_t)((ti >> 1) - 1) & 1u);
+        tc_fence_after();
+        const uint32_t dcol = tmem + (uint32_t)(buf * BNR);
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int slot = (int)(it % kSlots);
+          mbar_wait(xfull + slot, (it / kSlots) & 1u);
+          tc_fence_after();
+          const uint32_t wa = sbase + kOffW + kc * 2 * kImg;
+          const uint32_t xa = sbase + kOffX + slot * 2 * kImg;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t awh = umma_desc_sw128(wa + kk * 32);
+            const uint64_t awl = umma_desc_sw128(wa + kImg + kk * 32);
+            const uint64_t bxh = umma_desc_sw128(xa + kk * 32);
+            const uint64_t bxl = umma_desc_sw128(xa + kImg + kk * 32);
+            const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(dcol, awh, bxh, kIdesc, acc0);
+            mma_tf32(dcol, awl, bxh, kIdesc, 1u);
+            mma_tf32(dcol, awh, bxl, kIdesc, 1u);
+          }
+          mma_commit(xempty + slot);   // the slot is free once these MMAs have read it
+        }
+        mma_commit(tfull + buf);
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BNR)
+                 : "memory");
+  }
+}
+
+}  // namespace tc2
+
 size_t feature_map_tc_image_bytes(int r, int d) {
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
-  return (size_t)nt * nkc * 2 * tc::kWBytes;
+  const int nt2 = (r + tc2::BM - 1) / tc2::BM;
+  return std::max((size_t)nt * nkc * 2 * tc::kWBytes, (size_t)nt2 * nkc * 2 * tc2::kImg);
+}
+
+static int g_tc2_grid = 0;   // persistent grid (SM count), queried once
+
+template <int MODE>
+static cudaError_t launch_tc2(const float* X, int64_t n, int d, const float* wimg,
+                              const float* beta2, int r, float c2, float* Xi, int ld, int sdeg,
+                              cudaStream_t s) {
+  auto kern = tc2::feature_map_kernel<MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tc2::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (g_tc2_grid == 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_tc2_grid = sms;
+  }
+  const int ntn = (r + tc2::BM - 1) / tc2::BM;
+  const int64_t mtiles = (n + tc2::BNR - 1) / tc2::BNR;
+  int groups = std::max(1, g_tc2_grid / ntn);
+  groups = (int)std::min<int64_t>(groups, mtiles);
+  kern<<<groups * ntn, tc2::kThreads, tc2::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
@@ -280,6 +634,14 @@ cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float*
   if (ld <= 0) ld = r;
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
   const double wscale = mode == 0 ? 4.0 * tc::kLog2e / eps : 1.0;
+  if (nkc <= tc2::kMaxChunks) {   // persistent warp-specialised kernel, W block resident
+    const int nt2 = (r + tc2::BM - 1) / tc2::BM;
+    tc2::w_images_kernel<<<dim3(nt2, nkc), 256, 0, s>>>(U, r, d, wscale, wimg);
+    count_launch();
+    const float c2 = (float)(-2.0 * tc::kLog2e / eps);
+    return mode == 0 ? launch_tc2<0>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, s)
+                     : launch_tc2<1>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, s);
+  }
   tc::w_images_kernel<<<dim3(nt, nkc), 256, 0, s>>>(U, r, d, wscale, wimg);
   count_launch();
   cudaError_t e = cudaFuncSetAttribute(tc::feature_map_tc_kernel,
