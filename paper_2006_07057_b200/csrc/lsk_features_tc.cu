@@ -299,7 +299,10 @@ constexpr int BK = 32;              // k per chunk (one 128-byte swizzle row)
 constexpr int kMaxChunks = 4;       // d <= 128
 constexpr int kSlots = 2;
 constexpr int kImg = 128 * 128;     // bytes of one 128-row x 32-k tf32 image (16 KB)
-constexpr int kThreads = 288;       // 4 loader warps, 4 epilogue warps, 1 MMA warp
+constexpr int LW = 8;               // loader warps
+constexpr int NL = LW * 32;         // loader threads
+constexpr int JR = 1024 / NL;       // 16-byte quads per loader thread per chunk (128 rows x 8)
+constexpr int kThreads = (LW + 5) * 32;   // loaders, 4 epilogue warps, 1 MMA warp
 constexpr int kAlphaRing = 4;
 // smem: W images [nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | barriers
 constexpr int kOffW = 0;
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   const int64_t mtiles = (M + BNR - 1) / BNR;
   const int n0 = nt * BM;
 
-  if (warp == 8) {
+  if (warp == LW + 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)), "r"(2 * BNR)
                  : "memory");
@@ -360,14 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   if (tid == 0) {
     mbar_init(wbar, 1);
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(xfull + i, 128);
+      mbar_init(xfull + i, NL);
       mbar_init(xempty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
       mbar_init(tempty + i, 128);
     }
-    for (int i = 0; i < kAlphaRing; ++i) mbar_init(abar + i, 128);
+    for (int i = 0; i < kAlphaRing; ++i) mbar_init(abar + i, NL);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < LW) {
     // ------------------------------ loaders ---------------------------------------------
     if (tid == 0) {   // this CTA's anchor block of the W images, once
       const uint32_t bytes = (uint32_t)nkc * 2u * kImg;
@@ -388,17 +391,18 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
           "r"(smem_u32(wbar))
           : "memory");
     }
-    // thread t: 16-byte k-quad q = t % 8 of rows t / 8 + 16 j (j = 0..7) of the chunk
+    // thread t: 16-byte k-quad q = t % 8 of rows t / 8 + (NL / 8) j (j < JR) of the chunk
     const int q = tid & 7, rb = tid >> 3;
+    constexpr int RS = NL / 8;   // row stride between a thread's quads
     const bool vec = (d & 3) == 0;
     // the chunks of this CTA's tiles as one sequence; the next chunk's global loads are in
     // flight (registers) while the current one is split and stored
-    auto load_chunk = [&](int64_t mt, int kc, float4 (&v)[8]) {
+    auto load_chunk = [&](int64_t mt, int kc, float4 (&v)[JR]) {
       const int64_t m0 = mt * BNR;
       const int c0 = kc * BK + 4 * q;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int64_t row = m0 + rb + 16 * j;
+      for (int j = 0; j < JR; ++j) {
+        const int64_t row = m0 + rb + RS * j;
         v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row < M) {
           const float* src = X + row * d + c0;
@@ -416,32 +420,41 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
     int ti = 0;        // tiles so far (alpha ring)
     int64_t mt = grp;
     int kc = 0;
-    float xx[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    // a 3-deep register queue: chunks it+1 and it+2 are in flight while chunk it is split
-    float4 cur[8], n1[8], n2[8];
+    float xx[JR];
+#pragma unroll
+    for (int j = 0; j < JR; ++j) xx[j] = 0.f;
+    // a 4-deep register queue: chunks it+1 .. it+3 are in flight while chunk it is split
+    float4 cur[JR], n1[JR], n2[JR], n3[JR];
     auto advance = [&](int64_t& m, int& c) {
       if (++c == nkc) {
         c = 0;
         m += groups;
       }
     };
-    int64_t m1 = mt, m2;
-    int k1 = kc, k2;
+    // queue: cur = (mt, kc), then (m1, k1), (mq, kq), and (m2, k2) = the next to load
+    int64_t m1 = mt, mq, m2;
+    int k1 = kc, kq, k2;
     if (mt < mtiles) load_chunk(mt, 0, cur);
     advance(m1, k1);
     if (m1 < mtiles) load_chunk(m1, k1, n1);
-    m2 = m1;
-    k2 = k1;
+    mq = m1;
+    kq = k1;
+    advance(mq, kq);
+    if (mq < mtiles) load_chunk(mq, kq, n2);
+    m2 = mq;
+    k2 = kq;
     advance(m2, k2);
-    while (mt < mtiles) {
-      if (m2 < mtiles) load_chunk(m2, k2, n2);
+    // the loop body rotates the queue's roles (no register copies, which would wait for the
+    // loads just issued): step(cur, next, load-into)
+    auto step = [&](float4 (&cu)[JR], float4 (&ld2)[JR]) {
+      if (m2 < mtiles) load_chunk(m2, k2, ld2);
       const int slot = (int)(it % kSlots);
       if (it >= (uint32_t)kSlots) mbar_wait(xempty + slot, ((it / kSlots) - 1) & 1u);
       unsigned char* xs = smem + kOffX + slot * 2 * kImg;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < JR; ++j) {
         float4 hi, lo;
-        const float* e = &cur[j].x;
+        const float* e = &cu[j].x;
         float* h = &hi.x;
         float* l = &lo.x;
 #pragma unroll
@@ -450,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
           h[u] = tf32_rna(e[u]);
           l[u] = tf32_rna(e[u] - h[u]);
         }
-        const uint32_t off = swz128(rb + 16 * j, 4 * q);
+        const uint32_t off = swz128(rb + RS * j, 4 * q);
         *reinterpret_cast<float4*>(xs + off) = hi;
         *reinterpret_cast<float4*>(xs + kImg + off) = lo;
       }
@@ -460,12 +473,12 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
       if (kc == nkc - 1) {
         // alpha_i = c2 |x_i|^2: the 8 k-quads of a row are 8 consecutive lanes
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < JR; ++j) {
           float t = xx[j];
           t += __shfl_xor_sync(0xffffffffu, t, 1);
           t += __shfl_xor_sync(0xffffffffu, t, 2);
           t += __shfl_xor_sync(0xffffffffu, t, 4);
-          if (q == 0) alpha_s[(ti % kAlphaRing) * BNR + rb + 16 * j] = c2 * t;
+          if (q == 0) alpha_s[(ti % kAlphaRing) * BNR + rb + RS * j] = c2 * t;
           xx[j] = 0.f;
         }
         // ring entry ti % 4 is rewritten at tile ti + 4, after the MMAs of tile ti + 3, which
@@ -473,18 +486,24 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
         mbar_arrive(abar + (ti % kAlphaRing));
         ++ti;
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        cur[j] = n1[j];
-        n1[j] = n2[j];
-      }
       mt = m1;
       kc = k1;
-      m1 = m2;
-      k1 = k2;
+      m1 = mq;
+      k1 = kq;
+      mq = m2;
+      kq = k2;
       advance(m2, k2);
+    };
+    while (mt < mtiles) {
+      step(cur, n3);
+      if (mt >= mtiles) break;
+      step(n1, cur);
+      if (mt >= mtiles) break;
+      step(n2, n1);
+      if (mt >= mtiles) break;
+      step(n3, n2);
     }
-  } else if (warp < 8) {
+  } else if (warp < LW + 4) {
     // ------------------------------ epilogue --------------------------------------------
     const int qd = warp & 3;                    // TMEM lane quarter = anchors 32 qd ..
     const int k = n0 + 32 * qd + lane;          // this thread's anchor
@@ -587,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == LW + 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BNR)
                  : "memory");
