@@ -540,6 +540,8 @@ def run_lsk(args):
         alts = []
         if variant == "implicit" and "hybrid" in result["config"]["variant"]:
             alts.append(("implicit", -1.0))   # pure recompute (the hybrid's MUFU-only twin)
+        elif variant == "implicit" and cfg.r <= 1024 and cfg.d <= 3:
+            alts.append(("implicit", 0.25))   # the opt-in hybrid (MUFU + HBM) on the same workload
         alts.append(("stream" if variant == "implicit" else "implicit", 0.0))
         result["alt_variants"] = []
         for alt, sf in alts:

@@ -85,7 +85,8 @@ typedef struct lsk_solve_opts {
   double stream_fraction;  /* implicit solver only: fraction phi of each side's rows whose
                               factor rows are materialised once and streamed from HBM in every
                               pass while the rest are regenerated on the MUFU (both units busy
-                              in one launch).  0 = library default (0.25, DESIGN.md §6 K8),
+                              in one launch).  0 = library default (off: within 1% of the
+                              pure recompute kernel on config 2, DESIGN.md §6 K8),
                               < 0 = off (pure recompute),
                               in (0, 0.9] = that fraction.  Applies to r <= 1024, d <= 3, large
                               problems; phi (n + m) r 4 bytes of workspace. */

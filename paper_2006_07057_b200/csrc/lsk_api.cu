@@ -553,13 +553,13 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   return LSK_OK;
 }
 
-// Warp-specialised hybrid (lsk_hybrid.cu) default split: phi = 0.25 of each side's rows
-// streamed, measured on config 2 (us per pass, phi = off / 0.1 / 0.15 / 0.2 / 0.25 / 0.3:
-// 20.44 / 20.84 / 20.49 / 19.35 / 19.13 / 21.84 — past 0.25 the stream team sets the pace;
-// profiles/r02e_hybrid_sweep.log).  The rows beyond whole recompute rounds alone
-// (rows mod 32 SMs, phi 0.053) gained nothing: the recompute teams run ~20% slower per round
-// next to the stream team than alone.
-constexpr double kHybridDefault = 0.25;
+// Warp-specialised hybrid (lsk_hybrid.cu): off by default.  Its sweep (us per pass on config 2,
+// phi = off / 0.1 / 0.15 / 0.2 / 0.25 / 0.3: 20.44 / 20.84 / 20.49 / 19.35 / 19.13 / 21.84,
+// profiles/r02e_hybrid_sweep.log) did not hold under the bench protocol (an L2 flush before every
+// timed solve, interleaved arms, T = 200 and 500): phi = 0.25 runs at 20.33-20.35 us per pass
+// against 20.45 for the pure recompute kernel (scripts/ab_tc.py, profiles/r02_tmem_ex2_microbench.txt)
+// — within 1%, so the simpler kernel stays the default and phi > 0 is the caller's choice.
+constexpr double kHybridDefault = 0.0;
 
 // slot-0 bytes a solve carves besides the caller's own (the implicit row factors h_j of the
 // factored exponent); the solve state lives in slot 1, sized by run_solve after planning

@@ -114,6 +114,34 @@ def test_feature_map_matches_oracle(L, cfg_key, n):
     assert np.all(got >= 0)
 
 
+@pytest.mark.parametrize("d,r,n", [(40, 100, 1000), (100, 640, 129), (127, 256, 300),
+                                   (128, 512, 4099), (17, 132, 257), (128, 1000, 513)])
+def test_feature_map_tensor_core_shapes(L, d, r, n):
+    """The persistent tcgen05 feature map (d <= 128, DESIGN.md §6 K3): partial k chunks
+    (d % 32 != 0), the scalar load path (d % 4 != 0), partial anchor blocks (r % 128 != 0),
+    more anchor blocks than a cluster of SMs divides evenly (r = 640, 1000), ragged row tiles."""
+    import torch
+    rng = np.random.default_rng(d * 1000 + r)
+    X = (rng.normal(size=(n, d)) / math.sqrt(d)).astype(np.float32)
+    R = float(np.max(np.linalg.norm(X.astype(np.float64), axis=1)))
+    eps = 1.0
+    p = L.lsk_feature_params_init(eps, d, r, R, 4242)
+    U = torch.empty((r, d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.empty((n, r), dtype=torch.float32, device="cuda")
+    L.lsk_feature_map(p, U, _dev(X), Xi)
+    torch.cuda.synchronize()
+    prm = O.gaussian_params(eps, d, r, R)
+    Uo = O.draw_anchors(r, d, prm["sigma"], 4242)
+    ref = O.feature_matrix(X, Uo, eps, prm["q"]).T
+    got = Xi.cpu().double().numpy()
+    mask = ref > 1e-30
+    assert mask.mean() > 0.5
+    rel = np.abs(got[mask] - ref[mask]) / ref[mask]
+    assert rel.max() <= 1e-4, rel.max()
+    assert np.all(got[~mask] < 1e-29) and np.all(got >= 0)
+
+
 # ------------------------------------------------------------------ Sinkhorn parity ------
 def test_config1_full_streaming(L):
     cfg = synth.get_config(1)
