@@ -724,7 +724,7 @@ static lsk_status feature_map_impl(const lsk_feature_params* p, const float* U, 
                             bD, s));
   if (tensor) {
     LSK_CU(launch_feature_map_tc(X, rows, p->d, U, b2, p->r, p->eps,
-                                 reinterpret_cast<float*>(ws + oI), Xi, s));
+                                 reinterpret_cast<float*>(ws + oI), Xi, s, 0, 0, 0, p->R));
   } else {
     LSK_CU(launch_feature_map(X, rows, p->d, U, Wt, b2, bD, p->r, p->eps, Xi, s));
   }

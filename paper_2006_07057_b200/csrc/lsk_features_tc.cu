@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cuda_fp16.h>
+
 #include "lsk_internal.h"
 #include "lsk_ptx.cuh"
 
@@ -295,23 +297,82 @@ using tc::tc_fence_before;
 
 constexpr int BM = 128;             // anchors per CTA (MMA M)
 constexpr int BNR = 128;            // rows per tile (MMA N)
-constexpr int BK = 32;              // k per chunk (one 128-byte swizzle row)
-constexpr int kMaxChunks = 4;       // d <= 128
-constexpr int kSlots = 2;
-constexpr int kImg = 128 * 128;     // bytes of one 128-row x 32-k tf32 image (16 KB)
+constexpr int BK = 32;              // k per loader sub-chunk (the tf32 chunk)
+constexpr int kImg = 128 * 128;     // bytes of one 128-row x 128-byte image (16 KB)
 constexpr int LW = 8;               // loader warps
 constexpr int NL = LW * 32;         // loader threads
-constexpr int JR = 1024 / NL;       // 16-byte quads per loader thread per chunk (128 rows x 8)
+constexpr int JR = 1024 / NL;       // 16-byte quads per loader thread per sub-chunk
 constexpr int kThreads = (LW + 5) * 32;   // loaders, 4 epilogue warps, 1 MMA warp
 constexpr int kAlphaRing = 4;
-// smem: W images [nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | barriers
-constexpr int kOffW = 0;
-constexpr int kOffX = kOffW + kMaxChunks * 2 * kImg;
-constexpr int kOffAlpha = kOffX + kSlots * 2 * kImg;
-constexpr int kOffBar = kOffAlpha + kAlphaRing * BNR * 4;
-constexpr int kSmemBytes = kOffBar + 256 + 1024;   // + alignment slack
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BNR >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
+// Operand precision: H = false: 3xTF32 (hi/lo = cvt.rna.tf32), 32 k per 128-byte chunk row;
+// H = true: 3xFP16 on kind::f16 (twice the tf32 MMA rate, the same 11-bit significands), 64 k
+// per chunk row, operands pre-scaled by powers of two (x 2^sx from R, W 2^sw from max |W|) so
+// that they stay inside the fp16 range and the lo parts stay normal; the epilogue multiplies
+// the fp32 accumulator by 2^-(sx+sw) (exact).
+template <bool H>
+struct Cfg {
+  static constexpr int SUB = H ? 2 : 1;           // loader sub-chunks per MMA chunk
+  static constexpr int kMaxChunks = H ? 2 : 4;    // d <= 128
+  static constexpr int kSlots = H ? 4 : 2;
+  // smem: W images [nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | bars
+  static constexpr int kOffW = 0;
+  static constexpr int kOffX = kOffW + kMaxChunks * 2 * kImg;
+  static constexpr int kOffAlpha = kOffX + kSlots * 2 * kImg;
+  static constexpr int kOffBar = kOffAlpha + kAlphaRing * BNR * 4;
+  static constexpr int kSmemBytes = kOffBar + 256 + 1024;   // + alignment slack
+  // D = f32; A = B = tf32 (2) or f16 (0); both K-major; N = BNR, M = BM
+  static constexpr uint32_t kIdesc = (1u << 4) | ((H ? 0u : 2u) << 7) | ((H ? 0u : 2u) << 10) |
+                                     ((uint32_t)(BNR >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
+static_assert(Cfg<true>::kSmemBytes <= 227 * 1024 && Cfg<false>::kSmemBytes <= 227 * 1024, "smem");
+
+// byte offset of fp16 element (row, k) inside a K-major SWIZZLE_128B image (64 k per row)
+__host__ __device__ __forceinline__ uint32_t swz128h(int row, int k) {
+  const uint32_t chunk = (uint32_t)(k >> 3) ^ (uint32_t)(row & 7);
+  return (uint32_t)row * 128u + chunk * 16u + (uint32_t)(k & 7) * 2u;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// max |v| over n floats (non-negative float bits order as unsigned integers)
+__global__ void absmax_kernel(const float* __restrict__ v, int64_t n, unsigned int* out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(v[i]));
+  for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// fp16 W hi/lo images: [nt][kc][2][128 rows x 64 k x 2 B swizzled], W' = sc U 2^sw with
+// max |W'| ~ 2^14; block (0, 0) publishes the epilogue factor 2^-(sx + sw)
+__global__ void w_images_h_kernel(const float* __restrict__ U, int r, int d, double sc,
+                                  const unsigned int* __restrict__ amax, int sx,
+                                  float* __restrict__ img, float* __restrict__ fscale) {
+  const int nt = blockIdx.x, kc = blockIdx.y;
+  const int nkc = gridDim.y;
+  const double wmax = sc * (double)__uint_as_float(*amax);
+  const int sw = wmax > 0.0 ? max(-60, min(60, 14 - (int)ceil(log2(wmax)))) : 0;
+  const double s2 = sc * ldexp(1.0, sw);
+  char* base = reinterpret_cast<char*>(img) + ((size_t)nt * nkc + kc) * 2 * kImg;
+  for (int i = threadIdx.x; i < BM * 64; i += blockDim.x) {
+    const int row = i / 64, k = i % 64;
+    const int n = nt * BM + row, c = kc * 64 + k;
+    const float w = (n < r && c < d) ? (float)(s2 * (double)U[(int64_t)n * d + c]) : 0.f;
+    const __half hi = __float2half_rn(w);
+    const __half lo = __float2half_rn(w - __half2float(hi));
+    *reinterpret_cast<__half*>(base + swz128h(row, k)) = hi;
+    *reinterpret_cast<__half*>(base + kImg + swz128h(row, k)) = lo;
+  }
+  if (nt == 0 && kc == 0 && threadIdx.x == 0) *fscale = (float)ldexp(1.0, -(sx + sw));
+}
 
 // W hi/lo images for 128-anchor blocks: [nt][kc][2][128 rows x 128 B swizzled]
 __global__ void w_images_kernel(const float* __restrict__ U, int r, int d, double sc,
@@ -330,10 +391,14 @@ __global__ void w_images_kernel(const float* __restrict__ U, int r, int d, doubl
   }
 }
 
-template <int MODE>   // 0: Gaussian 2^(alpha + beta2 + G); 1: arc-cosine beta2 relu(G)^sdeg
+template <int MODE, bool H>   // MODE 0: Gaussian 2^(alpha + beta2 + G); 1: arc-cosine beta2 relu(G)^sdeg
 __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
     const float* __restrict__ X, int64_t M, int d, const float* __restrict__ wimg,
-    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int sdeg) {
+    const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int sdeg,
+    const float* __restrict__ fscale, float xscale) {
+  using C = Cfg<H>;
+  constexpr int kSlots = C::kSlots, kOffW = C::kOffW, kOffX = C::kOffX;
+  constexpr int kOffAlpha = C::kOffAlpha, kOffBar = C::kOffBar;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
@@ -350,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   const int ntn = (r + BM - 1) / BM;
   const int groups = gridDim.x / ntn;
   const int nt = blockIdx.x % ntn, grp = blockIdx.x / ntn;
-  const int nkc = (d + BK - 1) / BK;
+  const int nkc = (d + BK * C::SUB - 1) / (BK * C::SUB);   // MMA chunks (128-byte rows)
+  const int nsc = nkc * C::SUB;                             // loader sub-chunks per tile
   const int64_t mtiles = (M + BNR - 1) / BNR;
   const int n0 = nt * BM;
 
@@ -423,54 +489,68 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
     float xx[JR];
 #pragma unroll
     for (int j = 0; j < JR; ++j) xx[j] = 0.f;
-    // a 4-deep register queue: chunks it+1 .. it+3 are in flight while chunk it is split
-    float4 cur[JR], n1[JR], n2[JR], n3[JR];
+    // a 4-deep register queue: sub-chunks it+1 .. it+3 are in flight while sub-chunk it is split
+    // (two cursors: the sub-chunk being split, and the next one to load)
+    float4 q0[JR], q1[JR], q2[JR], q3[JR];
     auto advance = [&](int64_t& m, int& c) {
-      if (++c == nkc) {
+      if (++c == nsc) {
         c = 0;
         m += groups;
       }
     };
-    // queue: cur = (mt, kc), then (m1, k1), (mq, kq), and (m2, k2) = the next to load
-    int64_t m1 = mt, mq, m2;
-    int k1 = kc, kq, k2;
-    if (mt < mtiles) load_chunk(mt, 0, cur);
-    advance(m1, k1);
-    if (m1 < mtiles) load_chunk(m1, k1, n1);
-    mq = m1;
-    kq = k1;
-    advance(mq, kq);
-    if (mq < mtiles) load_chunk(mq, kq, n2);
-    m2 = mq;
-    k2 = kq;
-    advance(m2, k2);
+    int64_t mL = mt;
+    int kL = kc;
+    if (mL < mtiles) load_chunk(mL, kL, q0);
+    advance(mL, kL);
+    if (mL < mtiles) load_chunk(mL, kL, q1);
+    advance(mL, kL);
+    if (mL < mtiles) load_chunk(mL, kL, q2);
+    advance(mL, kL);
     // the loop body rotates the queue's roles (no register copies, which would wait for the
-    // loads just issued): step(cur, next, load-into)
+    // loads just issued): step(split this, load into that)
     auto step = [&](float4 (&cu)[JR], float4 (&ld2)[JR]) {
-      if (m2 < mtiles) load_chunk(m2, k2, ld2);
+      if (mL < mtiles) load_chunk(mL, kL, ld2);
+      advance(mL, kL);
       const int slot = (int)(it % kSlots);
-      if (it >= (uint32_t)kSlots) mbar_wait(xempty + slot, ((it / kSlots) - 1) & 1u);
+      const int sub = H ? (kc & 1) : 0;
+      if (sub == 0 && it >= (uint32_t)kSlots) mbar_wait(xempty + slot, ((it / kSlots) - 1) & 1u);
       unsigned char* xs = smem + kOffX + slot * 2 * kImg;
 #pragma unroll
       for (int j = 0; j < JR; ++j) {
-        float4 hi, lo;
         const float* e = &cu[j].x;
-        float* h = &hi.x;
-        float* l = &lo.x;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          xx[j] = fmaf(e[u], e[u], xx[j]);
-          h[u] = tf32_rna(e[u]);
-          l[u] = tf32_rna(e[u] - h[u]);
+        for (int u = 0; u < 4; ++u) xx[j] = fmaf(e[u], e[u], xx[j]);
+        if constexpr (H) {
+          const float x0 = e[0] * xscale, x1 = e[1] * xscale, x2 = e[2] * xscale, x3 = e[3] * xscale;
+          const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y);
+          const __half2 l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+          const uint32_t off = swz128h(rb + RS * j, 32 * sub + 4 * q);
+          *reinterpret_cast<uint2*>(xs + off) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+          *reinterpret_cast<uint2*>(xs + kImg + off) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+        } else {
+          float4 hi, lo;
+          float* h = &hi.x;
+          float* l = &lo.x;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            h[u] = tf32_rna(e[u]);
+            l[u] = tf32_rna(e[u] - h[u]);
+          }
+          const uint32_t off = swz128(rb + RS * j, 4 * q);
+          *reinterpret_cast<float4*>(xs + off) = hi;
+          *reinterpret_cast<float4*>(xs + kImg + off) = lo;
         }
-        const uint32_t off = swz128(rb + RS * j, 4 * q);
-        *reinterpret_cast<float4*>(xs + off) = hi;
-        *reinterpret_cast<float4*>(xs + kImg + off) = lo;
       }
-      fence_proxy_async_smem();
-      mbar_arrive(xfull + slot);
-      ++it;
-      if (kc == nkc - 1) {
+      if (sub == C::SUB - 1) {
+        fence_proxy_async_smem();
+        mbar_arrive(xfull + slot);
+        ++it;
+      }
+      if (kc == nsc - 1) {
         // alpha_i = c2 |x_i|^2: the 8 k-quads of a row are 8 consecutive lanes
 #pragma unroll
         for (int j = 0; j < JR; ++j) {
@@ -486,22 +566,16 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
         mbar_arrive(abar + (ti % kAlphaRing));
         ++ti;
       }
-      mt = m1;
-      kc = k1;
-      m1 = mq;
-      k1 = kq;
-      mq = m2;
-      kq = k2;
-      advance(m2, k2);
+      advance(mt, kc);
     };
     while (mt < mtiles) {
-      step(cur, n3);
+      step(q0, q3);
       if (mt >= mtiles) break;
-      step(n1, cur);
+      step(q1, q0);
       if (mt >= mtiles) break;
-      step(n2, n1);
+      step(q2, q1);
       if (mt >= mtiles) break;
-      step(n3, n2);
+      step(q3, q2);
     }
   } else if (warp < LW + 4) {
     // ------------------------------ epilogue --------------------------------------------
@@ -509,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
     const int k = n0 + 32 * qd + lane;          // this thread's anchor
     const bool kv = k < r;
     const float bk = kv ? beta2[k] : 0.f;
+    const float fs = H ? __ldg(fscale) : 1.f;   // 2^-(sx + sw): the operands' pre-scaling
     int ti = 0;
     for (int64_t mt = grp; mt < mtiles; mt += groups, ++ti) {
       const int64_t m0 = mt * BNR;
@@ -549,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
             const float* ap = &a4.x;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float acc = __uint_as_float(a[j + u]);
+              const float acc = H ? __uint_as_float(a[j + u]) * fs : __uint_as_float(a[j + u]);
               if (MODE == 0) {
                 o[j + u] = ex2((ap[u] + bk) + acc);
               } else {
@@ -587,15 +662,21 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
           const uint32_t wa = sbase + kOffW + kc * 2 * kImg;
           const uint32_t xa = sbase + kOffX + slot * 2 * kImg;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int kk = 0; kk < 4; ++kk) {   // 4 MMA k-steps of 32 bytes per 128-byte row
             const uint64_t awh = umma_desc_sw128(wa + kk * 32);
             const uint64_t awl = umma_desc_sw128(wa + kImg + kk * 32);
             const uint64_t bxh = umma_desc_sw128(xa + kk * 32);
             const uint64_t bxl = umma_desc_sw128(xa + kImg + kk * 32);
             const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(dcol, awh, bxh, kIdesc, acc0);
-            mma_tf32(dcol, awl, bxh, kIdesc, 1u);
-            mma_tf32(dcol, awh, bxl, kIdesc, 1u);
+            if constexpr (H) {
+              mma_f16(dcol, awh, bxh, C::kIdesc, acc0);
+              mma_f16(dcol, awl, bxh, C::kIdesc, 1u);
+              mma_f16(dcol, awh, bxl, C::kIdesc, 1u);
+            } else {
+              mma_tf32(dcol, awh, bxh, C::kIdesc, acc0);
+              mma_tf32(dcol, awl, bxh, C::kIdesc, 1u);
+              mma_tf32(dcol, awh, bxl, C::kIdesc, 1u);
+            }
           }
           mma_commit(xempty + slot);   // the slot is free once these MMAs have read it
         }
@@ -618,18 +699,19 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
 size_t feature_map_tc_image_bytes(int r, int d) {
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
   const int nt2 = (r + tc2::BM - 1) / tc2::BM;
-  return std::max((size_t)nt * nkc * 2 * tc::kWBytes, (size_t)nt2 * nkc * 2 * tc2::kImg);
+  // + 256 bytes: the fp16 path's max |U| and epilogue factor
+  return std::max((size_t)nt * nkc * 2 * tc::kWBytes, (size_t)nt2 * nkc * 2 * tc2::kImg) + 256;
 }
 
 static int g_tc2_grid = 0;   // persistent grid (SM count), queried once
 
-template <int MODE>
+template <int MODE, bool H>
 static cudaError_t launch_tc2(const float* X, int64_t n, int d, const float* wimg,
                               const float* beta2, int r, float c2, float* Xi, int ld, int sdeg,
-                              cudaStream_t s) {
-  auto kern = tc2::feature_map_kernel<MODE>;
+                              const float* fscale, float xscale, cudaStream_t s) {
+  auto kern = tc2::feature_map_kernel<MODE, H>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       tc2::kSmemBytes);
+                                       tc2::Cfg<H>::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (g_tc2_grid == 0) {
     int dev = 0, sms = 0;
@@ -641,32 +723,48 @@ static cudaError_t launch_tc2(const float* X, int64_t n, int d, const float* wim
   const int64_t mtiles = (n + tc2::BNR - 1) / tc2::BNR;
   int groups = std::max(1, g_tc2_grid / ntn);
   groups = (int)std::min<int64_t>(groups, mtiles);
-  kern<<<groups * ntn, tc2::kThreads, tc2::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg);
+  kern<<<groups * ntn, tc2::kThreads, tc2::Cfg<H>::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi,
+                                                                     ld, sdeg, fscale, xscale);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
                                   const float* beta2, int r, double eps, float* wimg, float* Xi,
-                                  cudaStream_t s, int mode, int sdeg, int ld) {
+                                  cudaStream_t s, int mode, int sdeg, int ld, double R) {
   if (n <= 0) return cudaSuccess;
   if (ld <= 0) ld = r;
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
   const double wscale = mode == 0 ? 4.0 * tc::kLog2e / eps : 1.0;
-  if (nkc <= tc2::kMaxChunks) {   // persistent warp-specialised kernel, W block resident
-    const int nt2 = (r + tc2::BM - 1) / tc2::BM;
+  const float c2 = (float)(-2.0 * tc::kLog2e / eps);
+  const int nt2 = (r + tc2::BM - 1) / tc2::BM;
+  if (mode == 0 && R > 0.0 && d <= 64 * tc2::Cfg<true>::kMaxChunks) {
+    // 3xFP16 (kind::f16): x scaled by 2^sx so that |x'| <= 2^12 for |x| <= 16 R
+    const int sx = std::max(-60, std::min(60, 12 - (int)std::ceil(std::log2(R))));
+    const int nkh = (d + 63) / 64;
+    char* scal = reinterpret_cast<char*>(wimg) + (size_t)nt2 * nkh * 2 * tc2::kImg;
+    unsigned int* amax = reinterpret_cast<unsigned int*>(scal);
+    float* fscale = reinterpret_cast<float*>(scal + 128);
+    cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    tc2::absmax_kernel<<<64, 256, 0, s>>>(U, (int64_t)r * d, amax);
+    count_launch();
+    tc2::w_images_h_kernel<<<dim3(nt2, nkh), 256, 0, s>>>(U, r, d, wscale, amax, sx, wimg, fscale);
+    count_launch();
+    return launch_tc2<0, true>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, fscale,
+                               (float)std::ldexp(1.0, sx), s);
+  }
+  if (nkc <= tc2::Cfg<false>::kMaxChunks) {   // 3xTF32, W block resident
     tc2::w_images_kernel<<<dim3(nt2, nkc), 256, 0, s>>>(U, r, d, wscale, wimg);
     count_launch();
-    const float c2 = (float)(-2.0 * tc::kLog2e / eps);
-    return mode == 0 ? launch_tc2<0>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, s)
-                     : launch_tc2<1>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, s);
+    return mode == 0 ? launch_tc2<0, false>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, nullptr, 1.f, s)
+                     : launch_tc2<1, false>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, nullptr, 1.f, s);
   }
   tc::w_images_kernel<<<dim3(nt, nkc), 256, 0, s>>>(U, r, d, wscale, wimg);
   count_launch();
   cudaError_t e = cudaFuncSetAttribute(tc::feature_map_tc_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemBytes);
   if (e != cudaSuccess) return e;
-  const float c2 = (float)(-2.0 * tc::kLog2e / eps);
   dim3 grid((unsigned)((n + tc::BM - 1) / tc::BM), (unsigned)nt);
   tc::feature_map_tc_kernel<<<grid, tc::kThreads, tc::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi,
                                                                         ld, mode, sdeg);

@@ -153,9 +153,11 @@ cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
                                double eps, float* Xi, cudaStream_t s);
 // tcgen05 3xTF32 feature map (lsk_features_tc.cu), used for d > 16
 size_t feature_map_tc_image_bytes(int r, int d);
+// R > 0 (the Gaussian map with a max-norm bound, d <= 128): 3xFP16 operands (kind::f16)
 cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float* U,
                                   const float* beta2, int r, double eps, float* wimg, float* Xi,
-                                  cudaStream_t s, int mode = 0, int sdeg = 0, int ld = 0);
+                                  cudaStream_t s, int mode = 0, int sdeg = 0, int ld = 0,
+                                  double R = 0.0);
 // arc-cosine features (NEXT f3)
 cudaError_t launch_arccos_coef(const float* U, int r, int d, double sigma, float* coef,
                                cudaStream_t s);

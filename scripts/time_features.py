@@ -42,7 +42,7 @@ ms = float(np.median(ts))
 out_bytes = 2 * X.shape[0] * cfg.r * 4
 flops = 3 * 2 * 2 * X.shape[0] * cfg.r * cfg.d
 print("feature map, both clouds (2 x %d x %d, d = %d): median %.3f ms (min %.3f); writes %.2f GB "
-      "-> %.0f GB/s; 3xTF32 %.1f TFLOP/s" % (X.shape[0], cfg.r, cfg.d, ms, min(ts), out_bytes / 1e9,
+      "-> %.0f GB/s; 3-term split GEMM %.1f TFLOP/s" % (X.shape[0], cfg.r, cfg.d, ms, min(ts), out_bytes / 1e9,
                                             out_bytes / ms / 1e6, flops / ms / 1e9))
 # sample check against the oracle (rows spread over the whole cloud, incl. the last tile)
 prm = O.gaussian_params(cfg.eps, cfg.d, cfg.r, 1.0)
