@@ -302,29 +302,35 @@ constexpr int kImg = 128 * 128;     // bytes of one 128-row x 128-byte image (16
 constexpr int LW = 8;               // loader warps
 constexpr int NL = LW * 32;         // loader threads
 constexpr int JR = 1024 / NL;       // 16-byte quads per loader thread per sub-chunk
-constexpr int kThreads = (LW + 5) * 32;   // loaders, 4 epilogue warps, 1 MMA warp
-constexpr int kAlphaRing = 4;
+
 // Operand precision: H = false: 3xTF32 (hi/lo = cvt.rna.tf32), 32 k per 128-byte chunk row;
 // H = true: 3xFP16 on kind::f16 (twice the tf32 MMA rate, the same 11-bit significands), 64 k
 // per chunk row, operands pre-scaled by powers of two (x 2^sx from R, W 2^sw from max |W|) so
 // that they stay inside the fp16 range and the lo parts stay normal; the epilogue multiplies
-// the fp32 accumulator by 2^-(sx+sw) (exact).
+// the fp32 accumulator by 2^-(sx+sw) (exact).  The fp16 W images are half the size, so an fp16
+// CTA keeps TWO 128-anchor blocks resident (MB = 2: 256 anchors, two MMAs per k-step, all 512
+// TMEM columns): every X tile it loads feeds twice the MMA work, and half as many CTAs load
+// each X tile.
 template <bool H>
 struct Cfg {
+  static constexpr int MB = H ? 2 : 1;            // 128-anchor blocks per CTA
   static constexpr int SUB = H ? 2 : 1;           // loader sub-chunks per MMA chunk
   static constexpr int kMaxChunks = H ? 2 : 4;    // d <= 128
-  static constexpr int kSlots = H ? 4 : 2;
-  // smem: W images [nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | bars
+  static constexpr int kSlots = H ? 3 : 2;
+  static constexpr int kAlphaRing = H ? 3 : 4;
+  // smem: W images [MB][nkc][2][kImg] | X slots [kSlots][2][kImg] | alpha [kAlphaRing][BNR] | bars
   static constexpr int kOffW = 0;
-  static constexpr int kOffX = kOffW + kMaxChunks * 2 * kImg;
+  static constexpr int kOffX = kOffW + MB * kMaxChunks * 2 * kImg;
   static constexpr int kOffAlpha = kOffX + kSlots * 2 * kImg;
   static constexpr int kOffBar = kOffAlpha + kAlphaRing * BNR * 4;
   static constexpr int kSmemBytes = kOffBar + 256 + 1024;   // + alignment slack
   // D = f32; A = B = tf32 (2) or f16 (0); both K-major; N = BNR, M = BM
   static constexpr uint32_t kIdesc = (1u << 4) | ((H ? 0u : 2u) << 7) | ((H ? 0u : 2u) << 10) |
                                      ((uint32_t)(BNR >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static constexpr int EW = 4 * MB;                // epilogue warps: one per (lane quarter, block)
+  static constexpr int kThreads = (LW + EW + 1) * 32;   // loaders, epilogue, 1 MMA warp
 };
-static_assert(Cfg<true>::kSmemBytes <= 227 * 1024 && Cfg<false>::kSmemBytes <= 227 * 1024, "smem");
+static_assert(Cfg<true>::kSmemBytes <= 232448 && Cfg<false>::kSmemBytes <= 232448, "smem");
 
 // byte offset of fp16 element (row, k) inside a K-major SWIZZLE_128B image (64 k per row)
 __host__ __device__ __forceinline__ uint32_t swz128h(int row, int k) {
@@ -392,13 +398,14 @@ __global__ void w_images_kernel(const float* __restrict__ U, int r, int d, doubl
 }
 
 template <int MODE, bool H>   // MODE 0: Gaussian 2^(alpha + beta2 + G); 1: arc-cosine beta2 relu(G)^sdeg
-__global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
+__global__ void __launch_bounds__(Cfg<H>::kThreads, 1) feature_map_kernel(
     const float* __restrict__ X, int64_t M, int d, const float* __restrict__ wimg,
     const float* __restrict__ beta2, int r, float c2, float* __restrict__ Xi, int ld, int sdeg,
     const float* __restrict__ fscale, float xscale) {
   using C = Cfg<H>;
   constexpr int kSlots = C::kSlots, kOffW = C::kOffW, kOffX = C::kOffX;
   constexpr int kOffAlpha = C::kOffAlpha, kOffBar = C::kOffBar;
+  constexpr int MB = C::MB, kAlphaRing = C::kAlphaRing, EW = C::EW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
@@ -412,17 +419,17 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + 2 * kSlots + kAlphaRing);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ntn = (r + BM - 1) / BM;
+  const int ntn = (r + MB * BM - 1) / (MB * BM);
   const int groups = gridDim.x / ntn;
   const int nt = blockIdx.x % ntn, grp = blockIdx.x / ntn;
   const int nkc = (d + BK * C::SUB - 1) / (BK * C::SUB);   // MMA chunks (128-byte rows)
   const int nsc = nkc * C::SUB;                             // loader sub-chunks per tile
   const int64_t mtiles = (M + BNR - 1) / BNR;
-  const int n0 = nt * BM;
+  const int n0 = nt * MB * BM;
 
-  if (warp == LW + 4) {
+  if (warp == LW + EW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)), "r"(2 * BNR)
+                     smem_u32(tmem_slot)), "r"(2 * MB * BNR)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -434,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, 128);
+      mbar_init(tempty + i, 32 * EW);
     }
     for (int i = 0; i < kAlphaRing; ++i) mbar_init(abar + i, NL);
     fence_mbar_init();
@@ -448,12 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   if (warp < LW) {
     // ------------------------------ loaders ---------------------------------------------
     if (tid == 0) {   // this CTA's anchor block of the W images, once
-      const uint32_t bytes = (uint32_t)nkc * 2u * kImg;
+      const uint32_t bytes = (uint32_t)(MB * nkc) * 2u * kImg;
       mbar_arrive_expect_tx(wbar, bytes);
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               sbase + kOffW),
-          "l"(reinterpret_cast<const char*>(wimg) + (size_t)nt * nkc * 2 * kImg), "r"(bytes),
+          "l"(reinterpret_cast<const char*>(wimg) + (size_t)nt * MB * nkc * 2 * kImg), "r"(bytes),
           "r"(smem_u32(wbar))
           : "memory");
     }
@@ -561,8 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
           if (q == 0) alpha_s[(ti % kAlphaRing) * BNR + rb + RS * j] = c2 * t;
           xx[j] = 0.f;
         }
-        // ring entry ti % 4 is rewritten at tile ti + 4, after the MMAs of tile ti + 3, which
-        // follow the epilogue's release of tile ti + 1's accumulator: alpha(ti) was read by then
+        // ring entry ti % kAlphaRing is rewritten at tile ti + kAlphaRing; the loader finishes
+        // that tile only after the MMAs of tile ti + kAlphaRing - 1 started, which follow the
+        // epilogue's release of tile ti (issued after its last read of alpha)
         mbar_arrive(abar + (ti % kAlphaRing));
         ++ti;
       }
@@ -577,12 +585,13 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
       if (mt >= mtiles) break;
       step(q3, q2);
     }
-  } else if (warp < LW + 4) {
+  } else if (warp < LW + EW) {
     // ------------------------------ epilogue --------------------------------------------
     const int qd = warp & 3;                    // TMEM lane quarter = anchors 32 qd ..
-    const int k = n0 + 32 * qd + lane;          // this thread's anchor
-    const bool kv = k < r;
-    const float bk = kv ? beta2[k] : 0.f;
+    const int mb = (warp - LW) >> 2;            // this warp's 128-anchor block
+    const int k = n0 + mb * BM + 32 * qd + lane;   // this thread's anchor
+    const bool kvm = k < r;
+    const float bkm = kvm ? beta2[k] : 0.f;
     const float fs = H ? __ldg(fscale) : 1.f;   // 2^-(sx + sw): the operands' pre-scaling
     int ti = 0;
     for (int64_t mt = grp; mt < mtiles; mt += groups, ++ti) {
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
 #pragma unroll 1
       for (int g = 0; g < BNR / 32; ++g) {
         uint32_t a[32];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(buf * BNR + 32 * g);
+        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)((buf * MB + mb) * BNR + 32 * g);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
             "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -607,17 +616,9 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
               "=r"(a[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (g == BNR / 32 - 1) {   // the buffer is drained: the next tile's MMAs may start
-          tc_fence_before();
-          mbar_arrive(tempty + buf);
-        }
         const int64_t rg = m0 + 32 * g;
-        if (kv) {
-          // one 64-bit base per 32-row group; rows as 32-bit offsets (32 ld < 2^31); a lane's
-          // store j and its neighbours' form 128 contiguous bytes of row rg + j
-          float* dst = Xi + rg * ld + k;
-          const int nrow = (M - rg) < 32 ? (int)(M - rg) : 32;
-          float o[32];
+        float o[32];
+        if (kvm) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 a4 = *reinterpret_cast<const float4*>(al + 32 * g + j);
@@ -626,13 +627,25 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
             for (int u = 0; u < 4; ++u) {
               const float acc = H ? __uint_as_float(a[j + u]) * fs : __uint_as_float(a[j + u]);
               if (MODE == 0) {
-                o[j + u] = ex2((ap[u] + bk) + acc);
+                o[j + u] = ex2((ap[u] + bkm) + acc);
               } else {
                 const float rl = fmaxf(acc, 0.f);
-                o[j + u] = bk * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
+                o[j + u] = bkm * (sdeg == 0 ? (acc > 0.f ? 1.f : 0.f) : (sdeg == 1 ? rl : rl * rl));
               }
             }
           }
+        }
+        // the tile's accumulator and alpha have been read: the next tile's MMAs may start (and,
+        // with them, the loader's reuse of this alpha entry)
+        if (g == BNR / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(tempty + buf);
+        }
+        if (kvm) {
+          // one 64-bit base per 32-row group; rows as 32-bit offsets (32 ld < 2^31); a lane's
+          // store j and its neighbours' form 128 contiguous bytes of row rg + j
+          float* dst = Xi + rg * ld + k;
+          const int nrow = (M - rg) < 32 ? (int)(M - rg) : 32;
           if (nrow == 32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) __stcs(dst + j * ld, o[j]);
@@ -654,28 +667,31 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
         const int buf = ti & 1;
         if (ti >= 2) mbar_wait(tempty + buf, (uint32_t)((ti >> 1) - 1) & 1u);
         tc_fence_after();
-        const uint32_t dcol = tmem + (uint32_t)(buf * BNR);
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const int slot = (int)(it % kSlots);
           mbar_wait(xfull + slot, (it / kSlots) & 1u);
           tc_fence_after();
-          const uint32_t wa = sbase + kOffW + kc * 2 * kImg;
           const uint32_t xa = sbase + kOffX + slot * 2 * kImg;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {   // 4 MMA k-steps of 32 bytes per 128-byte row
-            const uint64_t awh = umma_desc_sw128(wa + kk * 32);
-            const uint64_t awl = umma_desc_sw128(wa + kImg + kk * 32);
-            const uint64_t bxh = umma_desc_sw128(xa + kk * 32);
-            const uint64_t bxl = umma_desc_sw128(xa + kImg + kk * 32);
-            const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
-            if constexpr (H) {
-              mma_f16(dcol, awh, bxh, C::kIdesc, acc0);
-              mma_f16(dcol, awl, bxh, C::kIdesc, 1u);
-              mma_f16(dcol, awh, bxl, C::kIdesc, 1u);
-            } else {
-              mma_tf32(dcol, awh, bxh, C::kIdesc, acc0);
-              mma_tf32(dcol, awl, bxh, C::kIdesc, 1u);
-              mma_tf32(dcol, awh, bxl, C::kIdesc, 1u);
+          for (int mb = 0; mb < MB; ++mb) {
+            const uint32_t dcol = tmem + (uint32_t)((buf * MB + mb) * BNR);
+            const uint32_t wa = sbase + kOffW + (mb * nkc + kc) * 2 * kImg;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {   // 4 MMA k-steps of 32 bytes per 128-byte row
+              const uint64_t awh = umma_desc_sw128(wa + kk * 32);
+              const uint64_t awl = umma_desc_sw128(wa + kImg + kk * 32);
+              const uint64_t bxh = umma_desc_sw128(xa + kk * 32);
+              const uint64_t bxl = umma_desc_sw128(xa + kImg + kk * 32);
+              const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
+              if constexpr (H) {
+                mma_f16(dcol, awh, bxh, C::kIdesc, acc0);
+                mma_f16(dcol, awl, bxh, C::kIdesc, 1u);
+                mma_f16(dcol, awh, bxl, C::kIdesc, 1u);
+              } else {
+                mma_tf32(dcol, awh, bxh, C::kIdesc, acc0);
+                mma_tf32(dcol, awl, bxh, C::kIdesc, 1u);
+                mma_tf32(dcol, awh, bxl, C::kIdesc, 1u);
+              }
             }
           }
           mma_commit(xempty + slot);   // the slot is free once these MMAs have read it
@@ -687,9 +703,9 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == LW + 4) {
+  if (warp == LW + EW) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BNR)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * MB * BNR)
                  : "memory");
   }
 }
@@ -698,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) feature_map_kernel(
 
 size_t feature_map_tc_image_bytes(int r, int d) {
   const int nt = (r + tc::BN - 1) / tc::BN, nkc = (d + tc::BK - 1) / tc::BK;
-  const int nt2 = (r + tc2::BM - 1) / tc2::BM;
+  const int nt2 = (r + tc2::BM - 1) / tc2::BM + 1;   // + 1: the fp16 path pads to pairs of blocks
   // + 256 bytes: the fp16 path's max |U| and epilogue factor
   return std::max((size_t)nt * nkc * 2 * tc::kWBytes, (size_t)nt2 * nkc * 2 * tc2::kImg) + 256;
 }
@@ -719,11 +735,11 @@ static cudaError_t launch_tc2(const float* X, int64_t n, int d, const float* wim
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g_tc2_grid = sms;
   }
-  const int ntn = (r + tc2::BM - 1) / tc2::BM;
+  const int ntn = (r + tc2::Cfg<H>::MB * tc2::BM - 1) / (tc2::Cfg<H>::MB * tc2::BM);
   const int64_t mtiles = (n + tc2::BNR - 1) / tc2::BNR;
   int groups = std::max(1, g_tc2_grid / ntn);
   groups = (int)std::min<int64_t>(groups, mtiles);
-  kern<<<groups * ntn, tc2::kThreads, tc2::Cfg<H>::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi,
+  kern<<<groups * ntn, tc2::Cfg<H>::kThreads, tc2::Cfg<H>::kSmemBytes, s>>>(X, n, d, wimg, beta2, r, c2, Xi,
                                                                      ld, sdeg, fscale, xscale);
   count_launch();
   return cudaGetLastError();
@@ -742,14 +758,15 @@ cudaError_t launch_feature_map_tc(const float* X, int64_t n, int d, const float*
     // 3xFP16 (kind::f16): x scaled by 2^sx so that |x'| <= 2^12 for |x| <= 16 R
     const int sx = std::max(-60, std::min(60, 12 - (int)std::ceil(std::log2(R))));
     const int nkh = (d + 63) / 64;
-    char* scal = reinterpret_cast<char*>(wimg) + (size_t)nt2 * nkh * 2 * tc2::kImg;
+    const int nt2p = (nt2 + 1) & ~1;   // pairs of 128-anchor blocks (the pad block is zero)
+    char* scal = reinterpret_cast<char*>(wimg) + (size_t)nt2p * nkh * 2 * tc2::kImg;
     unsigned int* amax = reinterpret_cast<unsigned int*>(scal);
     float* fscale = reinterpret_cast<float*>(scal + 128);
     cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     tc2::absmax_kernel<<<64, 256, 0, s>>>(U, (int64_t)r * d, amax);
     count_launch();
-    tc2::w_images_h_kernel<<<dim3(nt2, nkh), 256, 0, s>>>(U, r, d, wscale, amax, sx, wimg, fscale);
+    tc2::w_images_h_kernel<<<dim3(nt2p, nkh), 256, 0, s>>>(U, r, d, wscale, amax, sx, wimg, fscale);
     count_launch();
     return launch_tc2<0, true>(X, n, d, wimg, beta2, r, c2, Xi, ld, sdeg, fscale,
                                (float)std::ldexp(1.0, sx), s);
