@@ -53,8 +53,13 @@ struct Smem {
   int mstop;      // multi-launch mode: the consumers stop at the top of this launch
 };
 
-template <int NV, int TR>
+// CW: columns per consumer group — 4 (float4 groups) or, for r <= 512 (fewer float4 groups than
+// consumer threads), 2 (float2 groups: every consumer thread owns columns, round 2; with float4
+// groups half the threads would load and multiply duplicate data, the per-tile cost of r = 1024
+// for half the bytes)
+template <int NV, int TR, int CW = 4>
 __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A) {
+  static_assert(CW == 4 || (CW == 2 && NV == 1), "float2 groups: one group per thread");
   extern __shared__ __align__(128) float ring[];
   __shared__ Smem S;
   constexpr int kFlushTiles = (32 / TR) > 0 ? (32 / TR) : 1;   // fp32 partial over <= 32 rows
@@ -165,16 +170,25 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
   }
 
   // ======================================= consumers ======================================
-  const int R4 = r >> 2;
+  const int RG = r / CW;   // column groups
   int g[NV];
   bool gv[NV];
   int ge[NV];   // clamped group index: invalid groups read column group 0 and use s = 0
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     g[j] = tid + j * NT;
-    gv[j] = g[j] < R4;
+    gv[j] = g[j] < RG;
     ge[j] = gv[j] ? g[j] : 0;
   }
+  // one column group of a feature row in shared memory (float2 groups: z, w = 0)
+  auto load_group = [](const float* rowp, int grp) -> float4 {
+    if constexpr (CW == 4) {
+      return *reinterpret_cast<const float4*>(rowp + 4 * grp);
+    } else {
+      const float2 v = *reinterpret_cast<const float2*>(rowp + 2 * grp);
+      return make_float4(v.x, v.y, 0.f, 0.f);
+    }
+  };
   float4 s[NV];
   double acc64[NV][4];
 #pragma unroll
@@ -262,8 +276,14 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
             double x[4];
-            cx_total4(cxtot, A.gpp, g[j], x);
-            s[j] = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+            if constexpr (CW == 4) {
+              cx_total4(cxtot, A.gpp, g[j], x);
+              s[j] = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+            } else {
+              cx_total4(cxtot, A.gpp, g[j] >> 1, x);
+              const int o = 2 * (g[j] & 1);
+              s[j] = make_float4((float)x[o], (float)x[o + 1], 0.f, 0.f);
+            }
           } else {
             s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
@@ -272,9 +292,14 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
-            const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j], multi);
-            const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j] + 2, multi);
-            s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+            if constexpr (CW == 4) {
+              const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j], multi);
+              const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j] + 2, multi);
+              s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
+            } else {
+              const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 2 * g[j], multi);
+              s[j] = make_float4((float)lo.x, (float)lo.y, 0.f, 0.f);
+            }
           } else {
             s[j] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
@@ -349,16 +374,17 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         for (int j = 0; j < NV; ++j) {
           float4 fvv[TR];
 #pragma unroll
-          for (int i = 0; i < TR; ++i)
-            fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+          for (int i = 0; i < TR; ++i) fvv[i] = load_group(feat + i * r, ge[j]);
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
             const float vi = vis[i];
             const float4 fv = fvv[i];
             acc32[j].x = fmaf(fv.x, vi, acc32[j].x);
             acc32[j].y = fmaf(fv.y, vi, acc32[j].y);
-            acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
-            acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
+            if constexpr (CW == 4) {
+              acc32[j].z = fmaf(fv.z, vi, acc32[j].z);
+              acc32[j].w = fmaf(fv.w, vi, acc32[j].w);
+            }
           }
         }
         if (++tiles_since_flush == kFlushTiles) {
@@ -402,14 +428,16 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
           float4 fvv[TR];
 #pragma unroll
           for (int i = 0; i < TR; ++i)   // all loads of this column group first
-            fvv[i] = *reinterpret_cast<const float4*>(feat + i * r + 4 * ge[j]);
+            fvv[i] = load_group(feat + i * r, ge[j]);
 #pragma unroll
           for (int i = 0; i < TR; ++i) {
             const float4 fv = fvv[i];
             pr[i] = fmaf(fv.x, s[j].x, pr[i]);
             pr[i] = fmaf(fv.y, s[j].y, pr[i]);
-            pr[i] = fmaf(fv.z, s[j].z, pr[i]);
-            pr[i] = fmaf(fv.w, s[j].w, pr[i]);
+            if constexpr (CW == 4) {
+              pr[i] = fmaf(fv.z, s[j].z, pr[i]);
+              pr[i] = fmaf(fv.w, s[j].w, pr[i]);
+            }
           }
         }
         const float tot = warp_transpose_reduce<TR>(pr, lane);
@@ -457,9 +485,9 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
         if (gv[j]) {
-          double2* d2 = reinterpret_cast<double2*>(cxpart + 4 * g[j]);
+          double2* d2 = reinterpret_cast<double2*>(cxpart + CW * g[j]);
           d2[0] = make_double2(acc64[j][0], acc64[j][1]);
-          d2[1] = make_double2(acc64[j][2], acc64[j][3]);
+          if constexpr (CW == 4) d2[1] = make_double2(acc64[j][2], acc64[j][3]);
         }
       }
       if (tid == 0) {
@@ -476,7 +504,15 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
       // R1: block partials part[blk][cta][4] (lsk_sink_common.cuh)
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
-        if (gv[j]) part_store4(part, A.gpp, g[j], cta, acc64[j][0], acc64[j][1], acc64[j][2], acc64[j][3]);
+        if (gv[j]) {
+          if constexpr (CW == 4) {
+            part_store4(part, A.gpp, g[j], cta, acc64[j][0], acc64[j][1], acc64[j][2], acc64[j][3]);
+          } else {   // half of block g/2: columns 2g, 2g+1
+            double2* d = reinterpret_cast<double2*>(part + ((((int64_t)(g[j] >> 1)) * A.gpp + cta) << 2) +
+                                                    2 * (g[j] & 1));
+            *d = make_double2(acc64[j][0], acc64[j][1]);
+          }
+        }
       }
       if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, e2, 0.0);
       group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
@@ -591,7 +627,7 @@ void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv) {
   int v = (r4 + NT - 1) / NT;
   int p2 = 1;
   while (p2 < v) p2 <<= 1;
-  *nv = p2;
+  *nv = (2 * r4 <= NT) ? 0 : p2;   // 0: one float2 group per consumer thread (r <= 512)
   // largest instantiated TR whose stage fits the budget (target 64 KB: long tiles amortise
   // the per-tile cross-warp exchange; measured on config 2: 32 KB stages 4.6 TB/s, 64 KB
   // stages 5.3 TB/s)
@@ -610,10 +646,10 @@ void sinkhorn_tile_config(int r, int max_stage_bytes, int* tr, int* nv) {
 
 size_t sinkhorn_static_smem() { return sizeof(Smem); }
 
-template <int NV, int TR>
+template <int NV, int TR, int CW = 4>
 static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
                             cudaStream_t s) {
-  auto kern = sinkhorn_kernel<NV, TR>;
+  auto kern = sinkhorn_kernel<NV, TR, CW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -642,29 +678,34 @@ static cudaError_t launch_t(const SinkArgs& a, bool coop, int grid, size_t smem,
   return e;
 }
 
-template <int NV, int TR>
+template <int NV, int TR, int CW = 4>
 static int occupancy_t(size_t smem) {
   int nb = 0;
-  auto kern = sinkhorn_kernel<NV, TR>;
+  auto kern = sinkhorn_kernel<NV, TR, CW>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
   return nb;
 }
 
+// nv = 0: NV = 1 with float2 column groups (r <= 512)
 #define LSK_STREAM_CASES(X) X(1, 32) X(1, 16) X(1, 8) X(2, 16) X(2, 8) X(2, 4) X(4, 8) X(4, 4) \
   X(4, 2) X(8, 4) X(8, 2) X(8, 1)
+#define LSK_STREAM_HALF_CASES(Y) Y(32) Y(16) Y(8)
 
 cudaError_t launch_sinkhorn(const SinkArgs& a, bool coop, int grid, size_t smem, cudaStream_t s) {
   const int tr = a.tr, nv = a.nv;
 #define X(NV_, TR_) if (nv == NV_ && tr == TR_) return launch_t<NV_, TR_>(a, coop, grid, smem, s);
   LSK_STREAM_CASES(X)
 #undef X
+#define Y(TR_) if (nv == 0 && tr == TR_) return launch_t<1, TR_, 2>(a, coop, grid, smem, s);
+  LSK_STREAM_HALF_CASES(Y)
+#undef Y
   return cudaErrorInvalidConfiguration;
 }
 
-template <int NV, int TR>
+template <int NV, int TR, int CW = 4>
 static int active_clusters_t(size_t smem, int csize) {
-  auto kern = sinkhorn_kernel<NV, TR>;
+  auto kern = sinkhorn_kernel<NV, TR, CW>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(csize);
@@ -689,6 +730,9 @@ int sinkhorn_max_active_clusters(int nv, int tr, size_t smem, int csize) {
 #define X(NV_, TR_) if (nv == NV_ && tr == TR_) return active_clusters_t<NV_, TR_>(smem, csize);
   LSK_STREAM_CASES(X)
 #undef X
+#define Y(TR_) if (nv == 0 && tr == TR_) return active_clusters_t<1, TR_, 2>(smem, csize);
+  LSK_STREAM_HALF_CASES(Y)
+#undef Y
   return 0;
 }
 
@@ -696,6 +740,9 @@ int sinkhorn_max_ctas_per_sm(int nv, int tr, size_t smem) {
 #define X(NV_, TR_) if (nv == NV_ && tr == TR_) return occupancy_t<NV_, TR_>(smem);
   LSK_STREAM_CASES(X)
 #undef X
+#define Y(TR_) if (nv == 0 && tr == TR_) return occupancy_t<1, TR_, 2>(smem);
+  LSK_STREAM_HALF_CASES(Y)
+#undef Y
   return 0;
 }
 
