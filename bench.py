@@ -211,7 +211,11 @@ def cpu_baseline(cfg, iters=3):
 MUFU_PEAK = 4626.0   # Gex2/s measured, profiles/r01_mufu_microbench.txt (16/clk/SM x 148 x 1.965 GHz = 4653)
 
 
-def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1, stream_rows=(0, 0)):
+SMEM_B_PER_CLK = 128.0   # shared-memory bandwidth per SM (B300_MICROARCH.md: 32 banks x 4 B)
+
+
+def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1, stream_rows=(0, 0),
+              resident=0):
     """Roofline object of the dominant kernel (the persistent Sinkhorn launch): algorithmic
     bytes (factor stream, HBM-bound) or ex2 (recompute, MUFU-bound) per launch over its mean
     CUDA-event duration.  The hybrid (a fraction of the rows streamed, the rest
@@ -219,6 +223,19 @@ def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1, stream_rows=(
     HBM bytes/s / 4 (factor entries/s)."""
     peaks, src = _peaks()
     ns0, ns1 = stream_rows
+    if resident:
+        # resident cluster kernel (DESIGN.md §6 K10): every pass reads its side's factor rows
+        # once from shared memory; the roof is the G SMs' shared-memory bandwidth (the
+        # one-time feature map of the implicit API is inside the timed launch window too)
+        rows = n_loc + T * (n_loc + m_loc)
+        alg_bytes = 4.0 * r * rows
+        achieved = alg_bytes / (kmean_ms / 1e3) / 1e9
+        peak = resident * SMEM_B_PER_CLK * float(peaks.get("sm_max_mhz", 1965.0)) / 1e3
+        return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "%d SMs x 128 B/clk x sm_max_mhz (%s)" % (resident, src),
+                "algorithmic_bytes_per_launch": alg_bytes, "cluster_ctas": resident,
+                "note": "one cluster barrier + DSMEM r-vector reduction per pass: latency-bound"}
     if var == "implicit" and ns0 + ns1 > 0:
         entries = float(r) * (n_loc + T * (n_loc + m_loc))
         streamed = float(r) * (ns0 + T * (ns0 + ns1))
@@ -366,6 +383,7 @@ def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True,
     v = torch.empty(m_loc, dtype=torch.float32, device=C.dev)
     opts = L.make_opts(T, stream_fraction=stream_fraction)
     srows = L.lsk_stream_rows(n_loc, m_loc, r, d, opts) if variant == "implicit" else (0, 0)
+    resident = L.lsk_resident_plan(n_loc, m_loc, r) if C.comm is None else 0
     stream = torch.cuda.current_stream()
     Xi = Ze = None
     if variant == "stream":
@@ -394,9 +412,11 @@ def measure_single(C, cfg, variant, scaling, steps, warmup, sample_clocks=True,
     tot_ms, kmean, launches, clk, rot = _timed_loop(C, step, steps, warmup, sample_clocks)
     out = {"value": T * steps / (tot_ms / 1e3), "unit": UNIT, "ms_per_step": tot_ms / steps,
            "kernel_ms": kmean, "gpu_launches": launches, "clocks": clk, "rot": rot,
-           "roofline": _roofline(variant, cfg.key, r, n_loc, m_loc, T, kmean, stream_rows=srows),
+           "roofline": _roofline(variant, cfg.key, r, n_loc, m_loc, T, kmean, stream_rows=srows,
+                                 resident=resident),
            "config": {"workload": "config%d-%s" % (cfg.key, cfg.name),
-                      "variant": variant + ("-hybrid" if srows[0] + srows[1] else ""),
+                      "variant": variant + ("-hybrid" if srows[0] + srows[1] else "")
+                                 + ("-resident%d" % resident if resident else ""),
                       "stream_rows": list(srows),
                       "global_n": gn, "global_m": gm, "n_per_gpu": n_loc, "m_per_gpu": m_loc,
                       "d": d, "r": r, "eps": eps, "T": T, "scaling": scaling,
@@ -606,7 +626,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="headline config: weak = N x the config's rows (pairs), strong = the "
                          "config's rows (pairs) split over the N GPUs")
-    ap.add_argument("--extra-configs", type=int, nargs="*", default=[3, 4, 5])
+    ap.add_argument("--extra-configs", type=int, nargs="*", default=[1, 3, 4, 5])
     ap.add_argument("--extra-steps", type=int, default=2)
     ap.add_argument("--no-extra", action="store_true", help="skip the configs 3/4/5 lines")
     ap.add_argument("--steps", type=int, default=5)

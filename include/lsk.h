@@ -81,7 +81,8 @@ typedef struct lsk_solve_opts {
   int32_t want_marginal_err;
   double tol;
   int32_t ctas_per_sm;     /* 0 = library default                                         */
-  int32_t flags;           /* LSK_SOLVE_STABILIZE: implicit solver in the row-normalised form */
+  int32_t flags;           /* LSK_SOLVE_STABILIZE: implicit solver in the row-normalised form;
+                              LSK_SOLVE_NO_RESIDENT: no resident small-problem kernel */
   double stream_fraction;  /* implicit solver only: fraction phi of each side's rows whose
                               factor rows are materialised once and streamed from HBM in every
                               pass while the rest are regenerated on the MUFU (both units busy
@@ -98,6 +99,12 @@ typedef struct lsk_solve_opts {
  * u~ = u e^A, v~ = v e^B of the normalised problem (lsk_implicit_row_offsets returns A, B) and
  * rep->rot is the value of the original problem (the offsets are folded in). */
 #define LSK_SOLVE_STABILIZE 1
+/* LSK_SOLVE_NO_RESIDENT: never use the resident small-problem kernel.  By default a
+ * single-GPU, single-problem solve whose factors fit in the shared memory of one thread-block
+ * cluster (<= 8 CTAs x 227 KB; r <= 512) keeps both factors on chip for the whole solve (the
+ * implicit solver then materialises them once); this flag forces the persistent grid kernels
+ * (same results within the parity tolerances; for tests and measurements). */
+#define LSK_SOLVE_NO_RESIDENT 2
 
 /* Report of one solve.  rot = W_hat of the returned (u, v);
  * marginal_err = |v o K^T u - b|_1 of the returned state, or -1 if not evaluated. */
@@ -370,6 +377,13 @@ lsk_status lsk_factored_sinkhorn_implicit_emulated(int32_t nranks, const lsk_fea
  * (lsk_factored_sinkhorn[_batched]), 2 = recompute (lsk_factored_sinkhorn_implicit*). */
 lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t batch,
                           int32_t variant, int32_t* gpp, int32_t* grid, int32_t* cluster);
+
+/* Diagnostic: the cluster size G (1, 2, 4 or 8 CTAs) of the resident small-problem kernel for a
+ * single-GPU, single-problem solve of this shape (both factors held in the CTAs' shared memory
+ * for the whole solve; DESIGN.md §6 K10), or 0 when the shape runs on the persistent grid
+ * kernels (r > 512, or the factors exceed 8 x 227 KB).  LSK_SOLVE_NO_RESIDENT forces the grid
+ * kernels; lsk_solve_plan describes those. */
+lsk_status lsk_resident_plan(int64_t n, int64_t m, int32_t r, int32_t* ctas);
 
 /* Diagnostic: the rows of each side (ns0 of X, ns1 of Y) that lsk_factored_sinkhorn_implicit
  * with these options materialises and streams from HBM (the warp-specialised hybrid kernel);

@@ -83,6 +83,7 @@ _SIGS = {
                                                         ctypes.c_void_p]),
     "lsk_solve_plan": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, P(c_i32), P(c_i32),
                                P(c_i32)]),
+    "lsk_resident_plan": (c_i32, [c_i64, c_i64, c_i32, P(c_i32)]),
     "lsk_lambert_w0": (c_i32, [ctypes.c_double, P(ctypes.c_double)]),
     "lsk_feature_params_init": (c_i32, [ctypes.c_double, c_i32, c_i32, ctypes.c_double,
                                         ctypes.c_uint64, c_f32p, c_i64, c_f32p, c_i64,
@@ -187,6 +188,14 @@ def lsk_stream_status(stream=None) -> int:
     return _check(_lib.lsk_stream_status(_stream(stream)), "lsk_stream_status")
 
 
+def lsk_resident_plan(n: int, m: int, r: int) -> int:
+    """Cluster CTAs of the resident small-problem kernel for this shape, 0 = grid kernels
+    (diagnostic; include/lsk.h)."""
+    g = c_i32()
+    _check(_lib.lsk_resident_plan(int(n), int(m), int(r), ctypes.byref(g)), "lsk_resident_plan")
+    return g.value
+
+
 def lsk_solve_plan(n: int, m: int, r: int, d: int, batch: int = 1, variant: str = "stream",
                    cluster: bool = False):
     """(gpp, grid) — and with cluster=True (gpp, grid, cluster) — of the launch a solve of this
@@ -239,15 +248,18 @@ def _stream(stream=None) -> int:
 
 
 LSK_SOLVE_STABILIZE = 1
+LSK_SOLVE_NO_RESIDENT = 2
 
 
 def make_opts(iters: int, tol: float = 0.0, want_err: bool = False,
               ctas_per_sm: int = 0, stabilize: bool = False,
-              stream_fraction: float = 0.0) -> lsk_solve_opts:
+              stream_fraction: float = 0.0, resident: bool = True) -> lsk_solve_opts:
     """stream_fraction (implicit solver): 0 = library default, < 0 = pure recompute,
-    (0, 0.9] = that fraction of rows streamed from HBM (include/lsk.h)."""
+    (0, 0.9] = that fraction of rows streamed from HBM (include/lsk.h).  resident=False:
+    never the resident small-problem kernel (LSK_SOLVE_NO_RESIDENT)."""
+    flags = (LSK_SOLVE_STABILIZE if stabilize else 0) | (0 if resident else LSK_SOLVE_NO_RESIDENT)
     return lsk_solve_opts(int(iters), 1 if want_err else 0, float(tol), int(ctas_per_sm),
-                          LSK_SOLVE_STABILIZE if stabilize else 0, float(stream_fraction))
+                          flags, float(stream_fraction))
 
 
 # ---------------------------------------------------------------- C-ABI mirrors ----------
@@ -561,7 +573,7 @@ def lsk_comm_enable_p2p(comm, r_max: int, stream=None):
 # ---------------------------------------------------------------- convenience -----------
 def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
         want_err=False, max_iters=None, ctas_per_sm=0, comm=None, stream=None, stabilize=False,
-        stream_fraction=0.0):
+        stream_fraction=0.0, resident=True):
     """Whole hot path on device tensors: a1 params -> a2 anchors -> a3 features -> Alg. 1 ->
     a9 read-out.  variant: "stream" (materialise xi, zeta) or "implicit" (recompute).
     stabilize=True: row-normalised features with log offsets (reading C30; stream: d <= 16,
@@ -578,7 +590,7 @@ def rot(X, Y, a, b, eps, r, seed, iters=None, tol=0.0, R=0.0, variant="stream",
     v = torch.empty(m, dtype=torch.float32, device=dev)
     T = iters if iters is not None else (max_iters or 1000)
     opts = make_opts(T, tol, want_err, ctas_per_sm, stabilize=stabilize and variant == "implicit",
-                     stream_fraction=stream_fraction)
+                     stream_fraction=stream_fraction, resident=resident)
     out = dict(params=p.as_dict(), U=U, u=u, v=v)
     if variant == "implicit":
         rep = lsk_factored_sinkhorn_implicit(p, U, X, Y, a, b, opts, u, v, comm=comm,

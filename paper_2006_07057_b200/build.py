@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblsk.so")
 SOURCES = ["lsk_api.cu", "lsk_features.cu", "lsk_features_tc.cu", "lsk_sinkhorn.cu", "lsk_implicit.cu",
-           "lsk_hybrid.cu", "lsk_grad.cu", "lsk_accel.cu"]
+           "lsk_hybrid.cu", "lsk_grad.cu", "lsk_accel.cu", "lsk_resident.cu"]
 TUNING_SOURCES = SOURCES + ["lsk_implicit_warp.cu", "lsk_implicit_tc.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

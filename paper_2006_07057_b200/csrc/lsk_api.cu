@@ -401,6 +401,35 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
   return LSK_OK;
 }
 
+constexpr int kPreDefault = 2;
+
+static lsk_status collect_reports(const SinkArgs& A, int batch, lsk_report* reps, bool nccl_rot,
+                                  cudaStream_t s);
+
+// Small single-GPU problems whose factors fit in the shared memory of one cluster (<= 8 CTAs):
+// the resident kernel (lsk_resident.cu, DESIGN.md §6 K10) instead of the persistent grid kernels
+static bool resident_allowed(const lsk_solve_opts* o) {
+  if (o && (o->flags & LSK_SOLVE_NO_RESIDENT)) return false;
+  const char* e = tuning_env("LSK_RESG");   // tuning knob: 0 = off
+  return !(e && atoi(e) == 0);
+}
+
+static int resident_pick(const SinkArgs& A, int batch, const lsk_comm* comm,
+                         const lsk_solve_opts* o) {
+  if (!resident_allowed(o) || batch != 1 || comm || A.emul || !A.F[0] || !A.F[1] || A.stab ||
+      A.nstream[0] + A.nstream[1] > 0)
+    return 0;
+  int G = resident_cluster(A.r, A.rows[0], A.rows[1]);
+  if (const char* e = tuning_env("LSK_RESG")) {   // tuning knob: 0 = off, else the cluster size
+    const int g = atoi(e);
+    if (g == 0) return 0;
+    if (G > 0 && (g == 1 || g == 2 || g == 4 || g == 8) &&
+        resident_smem_bytes(A.r, A.rows[0], A.rows[1], g) <= 227 * 1024)
+      G = g;
+  }
+  return G;
+}
+
 static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_opts* o,
                             lsk_report* reps, lsk_comm* comm, cudaStream_t s) {
   if (!o) return fail(LSK_EINVAL, "opts is NULL");
@@ -410,8 +439,30 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.tol = o->tol;
   A.want_err = (A.tol_mode || o->want_marginal_err) ? 1 : 0;
   A.num_passes = 2 * A.T + 1 + A.want_err;
+  if (const int G = resident_pick(A, batch, comm, o)) {
+    Carve sz;
+    const size_t oState = sz.take(sizeof(double) * kStateDoubles);
+    char* ws;
+    LSK_TRY(get_ws(s, sz.off, &ws, 1));
+    LSK_TRY(get_sticky(s, &A.sticky));
+    A.state = reinterpret_cast<double*>(ws + oState);
+    LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles, s));
+    A.nranks = 1;
+    A.rank = 0;
+    A.nprob = 1;
+    A.gpp = G;
+    A.pass_begin = 0;
+    A.pass_end = A.num_passes;
+    LSK_CU(launch_resident(A, G, 1, s));
+    return collect_reports(A, 1, reps, false, s);
+  }
   SolveCfg c;
   LSK_TRY(plan_solve(A, impl, batch, o, &c, !comm && !A.emul));
+  // implicit team kernel: the next pass's first feature tile is generated between the group
+  // barrier's arrive and wait (DESIGN.md §6 K5, boundary overlap; measured on the grid path
+  // only: the cluster boundary has no wait to hide it in)
+  A.pre = A.cx ? 0 : kPreDefault;
+  if (const char* e = tuning_env("LSK_PRE")) A.pre = std::max(0, std::min(2, atoi(e)));
   if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   const bool p2p = !A.emul && comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
                    !(getenv("LSK_P2P") && atoi(getenv("LSK_P2P")) == 0);
@@ -516,6 +567,13 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
     }
     cudaFree(trace);
   }
+  return collect_reports(A, batch, reps, comm && !p2p, s);
+}
+
+// reports of a finished solve (state blocks -> lsk_report), sticky status and weight /
+// breakdown / convergence statuses; nccl_rot: the read-out partials were all-reduced by NCCL
+static lsk_status collect_reports(const SinkArgs& A, int batch, lsk_report* reps, bool nccl_rot,
+                                  cudaStream_t s) {
   if (reps) {
     std::vector<double> st((size_t)kStateDoubles * batch);
     LSK_CU(cudaMemcpyAsync(st.data(), A.state, sizeof(double) * st.size(), cudaMemcpyDeviceToHost, s));
@@ -527,7 +585,7 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
       rp.iters = (int32_t)x[ST_ITERS];
       rp.converged = (int32_t)x[ST_CONV];
       rp.marginal_err = x[ST_ERR];
-      rp.rot = (comm && !p2p) ? A.eps * (x[ST_FINAL_A] + x[ST_FINAL_B]) : x[ST_ROT];
+      rp.rot = nccl_rot ? A.eps * (x[ST_FINAL_A] + x[ST_FINAL_B]) : x[ST_ROT];
       rp.sum_a_log_u = x[ST_FINAL_A];
       rp.sum_b_log_v = x[ST_FINAL_B];
       rp.breakdown = x[ST_BRK] > 0 ? 1 : 0;
@@ -606,6 +664,13 @@ lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t ba
   *gpp = c.gpp;
   *grid = c.grid;
   if (cluster) *cluster = A.cx;
+  return LSK_OK;
+}
+
+lsk_status lsk_resident_plan(int64_t n, int64_t m, int32_t r, int32_t* ctas) {
+  if (!ctas) return fail(LSK_EINVAL, "NULL argument");
+  LSK_TRY(check_common(n, m, r, 1.0));
+  *ctas = resident_cluster(r, n, m);
   return LSK_OK;
 }
 
@@ -889,15 +954,20 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
   int64_t ns0 = 0, ns1 = 0;
   if (hyb_ok) hybrid_rows(o, p->r, p->d, n, m, &ns0, &ns1);
   const bool hyb = ns0 + ns1 > 0;
-  const size_t oD = hyb ? cv.take(sizeof(float) * p->r) : 0;
-  const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r) : 0;
+  // small problems: the factors are materialised once (FFMA feature map) and the solve runs in
+  // the resident cluster kernel (run_solve -> resident_pick), which regenerates nothing
+  const bool res = !stab && !hyb && !tc_ok && !comm && resident_allowed(o) &&
+                   resident_cluster(p->r, n, m) > 0;
+  const size_t oD = (hyb || res) ? cv.take(sizeof(float) * p->r) : 0;
+  const size_t oF = hyb ? cv.take(sizeof(float) * (ns0 + ns1) * p->r)
+                        : (res ? cv.take(sizeof(float) * (n + m) * p->r) : 0);
 #ifdef LSK_TUNING
   const size_t oI = tc_ok ? cv.take(sizeof(float) * itc_image_floats(n + m)) : 0;
 #endif
   LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, 1), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
-  float* bD = hyb ? reinterpret_cast<float*>(ws + oD) : nullptr;
+  float* bD = (hyb || res) ? reinterpret_cast<float*>(ws + oD) : nullptr;
   LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, bD, s));
   SinkArgs A{};
   A.X[0] = X; A.X[1] = Y;
@@ -937,6 +1007,14 @@ lsk_status lsk_factored_sinkhorn_implicit(const lsk_feature_params* p, const flo
     A.F[1] = F1;
     A.nstream[0] = ns0;
     A.nstream[1] = ns1;
+  }
+  if (res) {
+    float* F0 = reinterpret_cast<float*>(ws + oF);
+    float* F1 = F0 + n * p->r;
+    LSK_CU(launch_feature_map(X, n, p->d, U, Wt, b2, bD, p->r, p->eps, F0, s));
+    LSK_CU(launch_feature_map(Y, m, p->d, U, Wt, b2, bD, p->r, p->eps, F1, s));
+    A.F[0] = F0;
+    A.F[1] = F1;
   }
   lsk_status st = run_solve(A, true, 1, o, rep, comm, s);
   if (stab && rep && st >= 0) {

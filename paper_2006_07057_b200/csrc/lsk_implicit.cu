@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
   double* sacc0 = reinterpret_cast<double*>(s_sm + NV * TS);   // [SW][GPL * 4][32] stream partials
   float* sring0 = reinterpret_cast<float*>(sacc0 + SW * GPL * 4 * 32);   // [SW][kSRing][kSRow]
   double* cxtot = reinterpret_cast<double*>(sring0 + SW * kSRing * kSRow);  // cx: [(r/4+1)*4]
+  float4* stash4 = reinterpret_cast<float4*>(cxtot + (A.cx ? ((A.r >> 2) + 1) * 4 : 0));   // [TR*NV][NT]
   uint32_t cxphase = 0;
 
   const int tid = threadIdx.x;
@@ -386,6 +387,83 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
     }
   };
 
+  // one tile's features of this thread's columns: F_jk (or G_jk) = 2^(exponent) for the TR
+  // staged point rows of slot sl (independent of s: also generated ahead, across a boundary)
+  auto gen_features = [&](const float* sl, float2 (&fr)[TR][NV][2]) {
+#pragma unroll
+    for (int i = 0; i < TR; ++i) {
+      float x[XS];
+      {
+        const float4 x0 = lds128(sl + 96 + i * XS);
+        x[0] = x0.x; if (XS > 1) x[1] = x0.y;
+        if (XS > 2) x[2] = x0.z;
+        if (XS > 3) x[3] = x0.w;
+        if constexpr (XS > 4) {
+          const float4 x1 = lds128(sl + 96 + i * XS + 4);
+          x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
+        }
+      }
+      float2 al2 = make_float2(0.f, 0.f);
+      if constexpr (STAB) {
+        const float mj = -sl[32 + i];   // the row's shift: every G_jk <= ~1
+        al2 = make_float2(mj, mj);
+      } else if constexpr (!FACT) {
+        float al = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
+        al *= A.c2;
+        al2 = make_float2(al, al);
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);   // STAB: al2 = -m_j
+#pragma unroll
+          for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
+          fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
+        }
+      }
+    }
+  };
+  // boundary overlap (DESIGN.md §6 K5): tile 0 of the next pass is generated while the CTA
+  // waits at the pass boundary and parked in shared memory (element-major: conflict-free
+  // 128-bit stores and loads); pre_done: the stash holds this pass's tile 0
+  constexpr bool kPre = !PIPE && SW == 0;
+  bool pre_done = false;
+  auto stash_store = [&](const float2 (&fr)[TR][NV][2]) {
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        stash4[(i * NV + j) * NT + tid] = make_float4(fr[i][j][0].x, fr[i][j][0].y, fr[i][j][1].x, fr[i][j][1].y);
+  };
+  auto stash_load = [&](float2 (&fr)[TR][NV][2]) {
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const float4 v = stash4[(i * NV + j) * NT + tid];
+        fr[i][j][0] = make_float2(v.x, v.y);
+        fr[i][j][1] = make_float2(v.z, v.w);
+      }
+  };
+  // generate the features of pass q's tile 0 into the stash (its slot was issued when this pass's
+  // tiles ended); A.pre = 1: after R2, 2: between the group barrier's arrive and wait
+  auto pre_gen = [&](int q) {
+    if constexpr (kPre) {
+      if (q >= A.pass_end || pass_kind(q, A) == PK_NONE) return;
+      const int nr = rcnt[(pass_kind(q, A) == PK_V || pass_kind(q, A) == PK_ERR) ? 1 : 0];
+      if (team * TR >= nr) return;   // this team has no tile in pass q
+      if (twarp == 0) cp_async_wait<kAhead - 1>();   // tile 0 landed
+      named_bar(team_bar, TS);
+      float2 fr[TR][NV][2];
+      gen_features(tslots + (gt % kRing) * SLOT, fr);
+      stash_store(fr);
+      pre_done = true;
+    }
+  };
+
   for (int p = A.pass_begin;; ++p) {
     // ---------------- results of pass q = p-1: stopping test (see lsk_sinkhorn.cu) -------
     const bool have_prev = multi ? (p == A.pass_begin && p > 0) : (p > A.pass_begin);
@@ -495,51 +573,23 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
 #pragma unroll
           for (int t = 0; t < kAhead; ++t) issue(t);
         }
-        if constexpr (!PIPE) cp_async_wait<kAhead - 1>();   // tile 0 landed
+        if constexpr (!PIPE) {
+          if (!pre_done) cp_async_wait<kAhead - 1>();   // tile 0 landed
+        }
       }
-      if constexpr (!PIPE) named_bar(team_bar, TS);
+      if constexpr (!PIPE) {
+        if (!pre_done) named_bar(team_bar, TS);
+      }
 
       // generate tile t's features into fr and publish its row-dot partials
-      auto compute = [&](int t, float2 (&fr)[TR][NV][2]) {
+      // GEN = false: fr already holds the tile (generated at the previous pass boundary)
+      auto compute = [&](int t, float2 (&fr)[TR][NV][2], auto gen_tag) {
         if (twarp == 0) issue(t + kAhead);
         const uint32_t gi = gt0 + (uint32_t)t;
         const float* sl = tslots + (gi % kRing) * SLOT;
         if constexpr (PIPE) mbar_wait(&S.full[team][gi % kRing], (gi / kRing) & 1u);
-#pragma unroll
-        for (int i = 0; i < TR; ++i) {
-          float x[XS];
-          {
-            const float4 x0 = lds128(sl + 96 + i * XS);
-            x[0] = x0.x; if (XS > 1) x[1] = x0.y;
-            if (XS > 2) x[2] = x0.z;
-            if (XS > 3) x[3] = x0.w;
-            if constexpr (XS > 4) {
-              const float4 x1 = lds128(sl + 96 + i * XS + 4);
-              x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
-            }
-          }
-          float2 al2 = make_float2(0.f, 0.f);
-          if constexpr (STAB) {
-            const float mj = -sl[32 + i];   // the row's shift: every G_jk <= ~1
-            al2 = make_float2(mj, mj);
-          } else if constexpr (!FACT) {
-            float al = 0.f;
-#pragma unroll
-            for (int c = 0; c < D; ++c) al = fmaf(x[c], x[c], al);
-            al *= A.c2;
-            al2 = make_float2(al, al);
-          }
-#pragma unroll
-          for (int j = 0; j < NV; ++j) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              float2 e = FACT ? B2[j][h] : add2(al2, B2[j][h]);   // STAB: al2 = -m_j
-#pragma unroll
-              for (int c = 0; c < D; ++c) e = fma2(W2[j][c][h], make_float2(x[c], x[c]), e);
-              fr[i][j][h] = make_float2(ex2(e.x), ex2(e.y));
-            }
-          }
-        }
+        if constexpr (decltype(gen_tag)::value) gen_features(sl, fr);
+        else stash_load(fr);
         const int rb = (int)(gi % 3u);
         if constexpr (kDot) {
           float pr[TR];
@@ -631,26 +681,35 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         }
       };
 
-      float2 frA[TR][NV][2];
       if constexpr (PIPE) {
+        float2 frA[TR][NV][2];
         float2 frB[TR][NV][2];
         if (ntiles > 0) {
           int t = 0;
-          compute(0, frA);
+          compute(0, frA, std::true_type{});
           while (true) {   // frA holds tile t
             if (t + 1 >= ntiles) { finish(t, frA); break; }
-            compute(t + 1, frB);
+            compute(t + 1, frB, std::true_type{});
             finish(t, frA);
             ++t;           // frB holds tile t
             if (t + 1 >= ntiles) { finish(t, frB); break; }
-            compute(t + 1, frA);
+            compute(t + 1, frA, std::true_type{});
             finish(t, frB);
             ++t;
           }
         }
       } else {
-        for (int t = 0; t < ntiles; ++t) {
-          compute(t, frA);
+        float2 frA[TR][NV][2];
+        int t0 = 0;
+        if constexpr (kPre) {
+          if (pre_done && ntiles > 0) {   // tile 0 from the stash (peeled: the loop always generates)
+            compute(0, frA, std::false_type{});
+            finish(0, frA);
+            t0 = 1;
+          }
+        }
+        for (int t = t0; t < ntiles; ++t) {
+          compute(t, frA, std::true_type{});
           finish(t, frA);
         }
       }
@@ -665,6 +724,19 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         default: run_tiles(std::integral_constant<int, PK_ERR>{}); break;
       }
       gt += (uint32_t)ntiles;
+      pre_done = false;
+      if constexpr (!PIPE && SW == 0) {
+        // boundary overlap: the next pass's first tiles are issued now (their slots are free),
+        // so they have landed when the team generates tile 0's features at the boundary
+        if (A.pre && twarp == 0) {
+          const int q = p + 1;
+          if (q < A.pass_end && pass_kind(q, A) != PK_NONE) {
+            const Feed nf = make_feed(q);
+#pragma unroll
+            for (int t = 0; t < kAhead; ++t) issue_tile(nf, gt, t);
+          }
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -765,7 +837,19 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         }
       }
       if (tid == 0) part_store4(part, A.gpp, r >> 2, cta, e0, e1, e2, 0.0);
-      group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      if (A.pre == 2) {   // the group barrier, with the next tile's features between arrive and wait
+        named_bar(1, NT);
+        if (tid == 0) red_release_add(A.bar + prob, 1u);
+        ++nbar;
+        pre_gen(p + 1);
+        if (tid == 0) {
+          while (ld_acquire(A.bar + prob) < nbar * (unsigned)A.gpp) {
+          }
+        }
+        named_bar(1, NT);
+      } else {
+        group_barrier<NT>(A.bar + prob, (++nbar) * (unsigned)A.gpp, tid);
+      }
       if (trc) trc[1] = globaltimer();
       // R2: this CTA reduces column blocks kb = cta, cta+gpp, ... (block r/4: the extras)
       r2_cta(A, prob, p, part, cta, warp, NW, lane);
@@ -786,7 +870,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
     if constexpr (!PIPE) {
       const int q = p + 1;
       if (q < A.pass_end && pass_kind(q, A) != PK_NONE) {
-        if (!strm && twarp == 0) {
+        if (!strm && twarp == 0 && !A.pre) {
           const Feed nf = make_feed(q);
 #pragma unroll
           for (int t = 0; t < kAhead; ++t) issue_tile(nf, gt, t);
@@ -794,6 +878,8 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         prefetched = true;
       }
     }
+    // boundary overlap (after this CTA's share of R2, while the other owners finish theirs)
+    if (A.pre && !strm && !pre_done) pre_gen(p + 1);
   }
 
   if constexpr (!PIPE) {
@@ -935,11 +1021,12 @@ __global__ void __launch_bounds__(256) row_shift_kernel(const float* __restrict_
   A[j] = ((double)(al * c2) + (double)mx) * 0.69314718055994530942;
 }
 
-template <int TS, int TEAMS, int NV, int TR, int D, int SW = 0>
+template <int TS, int TEAMS, int NV, int TR, int D, int SW = 0, bool PIPE = false>
 constexpr size_t dyn_smem() {
   return sizeof(double) * NV * 4 * (TS * TEAMS + 32 * SW) +
          sizeof(float) * TEAMS * kRing * Geo<D>::SLOT + sizeof(float4) * NV * TS +
-         sizeof(double) * SW * NV * TS * 4 + sizeof(float) * SW * kSRing * kSRow;
+         sizeof(double) * SW * NV * TS * 4 + sizeof(float) * SW * kSRing * kSRow +
+         ((!PIPE && SW == 0) ? sizeof(float4) * TR * NV * TS * TEAMS : 0);   // boundary stash
 }
 
 }  // namespace impl
@@ -997,7 +1084,9 @@ ImplCfg implicit_config(int r, int d) {
   LSK_IMPL_D(X, 128, 4, 2, 4, 0) LSK_IMPL_D(X, 512, 1, 1, 8, 0)                           \
   LSK_IMPL_D(X, 512, 1, 2, 4, 0) LSK_IMPL_D123(X, 128, 2, 2, 16, 0)                       \
   LSK_IMPL_D123(X, 256, 1, 4, 8, 0)
-#ifdef LSK_TUNING
+#if defined(LSK_AB_ONLY)   // quick A/B builds: the config 1, 2 and 5 kernels only
+#define LSK_IMPL_ALL(X) X(32, 8, 1, 16, 0, 2) X(128, 2, 2, 16, 0, 2) X(256, 1, 4, 8, 0, 3)
+#elif defined(LSK_TUNING)
 #define LSK_IMPL_ALL(X) LSK_IMPL_DEFAULT(X) LSK_IMPL_D23(X, 128, 2, 2, 8, 1) \
   LSK_IMPL_D23(X, 256, 1, 4, 2, 1) X(128, 3, 2, 8, 0, 2) LSK_IMPL_EXTRA(X)
 #ifdef LSK_IMPL_EXTRA_H
@@ -1017,7 +1106,7 @@ static size_t cx_smem(const SinkArgs& a) {
 template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
 static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream_t s) {
   auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE, SW>;
-  const size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>() + cx_smem(a);
+  const size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW, PIPE>() + cx_smem(a);
   constexpr int nthr = TS * TM + 32 * SW;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
@@ -1049,7 +1138,7 @@ static cudaError_t launch_cfg(const SinkArgs& a, bool coop, int grid, cudaStream
 template <int TS, int TM, int NV, int TR, int D, int MODE, bool PIPE, int SW = 0>
 static int occupancy_cfg() {
   auto kern = impl::implicit_kernel<TS, TM, NV, TR, D, MODE, PIPE, SW>;
-  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW>();
+  constexpr size_t dyn = impl::dyn_smem<TS, TM, NV, TR, D, SW, PIPE>();
   int nb = 0;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TS * TM + 32 * SW, dyn);

@@ -96,6 +96,8 @@ struct SinkArgs {
   int emul;                // 1: the nprob problems of this launch are the nranks ranks of ONE
                            // row-sharded solve (rank = problem index; xbox[] all on this GPU):
                            // the cross-GPU exchange emulated inside one cooperative launch
+  int pre;                 // implicit team kernel: generate the next pass's first feature tile
+                           // at the pass boundary (0 off, 1 after R2, 2 inside the barrier)
 };
 
 // Kernel launchers (lsk_sinkhorn.cu).  Return cudaError_t of the launch.
@@ -139,6 +141,12 @@ cudaError_t launch_row_shift(const float* X, int64_t n, int d, const float* Wt,
 // h_j = 2^(c2 |p_j|^2 - abar) for the factored exponent (one launch per solve and side)
 cudaError_t launch_row_scale(const float* X, int64_t n, int d, float c2, float abar, float* h,
                              cudaStream_t s);
+
+// Resident small-problem kernel (lsk_resident.cu): both factors in the shared memory of one
+// cluster of G <= 8 CTAs per problem; resident_cluster returns 0 when they do not fit
+size_t resident_smem_bytes(int r, int64_t n, int64_t m, int G);
+int resident_cluster(int r, int64_t n, int64_t m);
+cudaError_t launch_resident(const SinkArgs& a, int G, int batch, cudaStream_t s);
 
 // Feature kernels (lsk_features.cu)
 cudaError_t launch_max_sqnorm(const float* X, int64_t n, int d, unsigned long long* out,

@@ -231,12 +231,14 @@ def test_cluster_mode_small_problems(L, variant, n, m, T):
     assert cx == 1 and 2 <= gpp <= 8 and grid == gpp, (gpp, grid, cx)
     prob = synth.make_problem(cfg, n=n, m=m)
     X, Y, a, b = (_dev(prob[k]) for k in ("X", "Y", "a", "b"))
-    res = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T, variant=variant)
+    # resident=False: these shapes would otherwise run on the resident kernel (test_gpu_resident)
+    res = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, iters=T, variant=variant,
+                resident=False)
     ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, T=T)
     _parity(res["u"], res["v"], res["rot"], ref)
     # tolerance mode: the stop decision from the cluster totals
     res_t = L.rot(X, Y, a, b, cfg.eps, cfg.r, cfg.anchor_seed, max_iters=500, tol=1e-6,
-                  variant=variant)
+                  variant=variant, resident=False)
     ref_t = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], cfg.eps, cfg.r, cfg.anchor_seed, tol=1e-6)
     assert res_t["report"]["converged"] == 1 and abs(res_t["report"]["iters"] - ref_t["iters"]) <= 1
 
