@@ -139,6 +139,13 @@ __device__ __forceinline__ double ld_dsmem_f64(uint32_t cluster_addr) {
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
   return v;
 }
+// remote shared-memory store that completes tx bytes on the destination CTA's mbarrier
+// (both addresses shared::cluster, from mapa)
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "d"(v), "r"(cluster_mbar)
+               : "memory");
+}
 __device__ __forceinline__ double2 ld_dsmem_v2f64(uint32_t cluster_addr) {
   double2 v;
   asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(cluster_addr)

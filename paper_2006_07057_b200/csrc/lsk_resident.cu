@@ -16,10 +16,13 @@
 // the float4 column groups l + 32 i (i < NG).  Row dots: lane partials + a warp transpose-reduce
 // (lanes 4k..4k+3 end with row k's total; fixed shuffle order).  Accumulation: fp32 over <= 64
 // rows, then fp64 per lane; warp partials -> CTA partial in fixed warp order (fp64, shared
-// memory, double-buffered by pass parity) -> every CTA sums the G CTA partials in CTA order over
-// DSMEM (identical bits in every CTA, so every CTA takes the same stopping decision without a
-// broadcast).  One cluster barrier per pass: a CTA rewrites its parity-p partial only at pass
-// p + 2, after barrier p + 1, which every reader of pass p passed after reading it.
+// memory) -> pushed with st.async into slot [p & 1][cta] of EVERY CTA's receive buffer,
+// completing bytes on the receiver's parity-(p & 1) mbarrier -> every CTA waits on its own
+// mbarrier and sums the G slots in CTA order (identical bits in every CTA, so every CTA takes
+// the same stopping decision without a broadcast).  No cluster barrier per pass: the sender of
+// pass p + 2's partial has received every CTA's pass p + 1 partial, so every CTA had finished
+// reading its pass-p slots.  Breakdown and bad-weight counts only matter for the report: they
+// stay per thread until the end; only the marginal error is summed every pass.
 #include <algorithm>
 #include <cmath>
 
@@ -39,8 +42,8 @@ __host__ __device__ inline size_t up16(size_t x) { return (x + 15) & ~size_t(15)
 
 // dynamic shared memory layout (bytes), identical on host and device
 struct Lay {
-  size_t F0, F1, c0, c1, u, v, s32, wp, cp, tot, xs, rdo, total;
-  __host__ __device__ Lay(int r, int n0, int n1) {
+  size_t F0, F1, c0, c1, u, v, s32, wp, rb, tot, xs, rdo, bar, total;
+  __host__ __device__ Lay(int r, int n0, int n1, int G) {
     size_t o = 0;
     F0 = o; o += up16(sizeof(float) * (size_t)n0 * r);
     F1 = o; o += up16(sizeof(float) * (size_t)n1 * r);
@@ -50,10 +53,11 @@ struct Lay {
     v = o;  o += up16(sizeof(float) * 2 * (size_t)n1);        // v by iteration parity
     s32 = o; o += up16(sizeof(float) * r);
     wp = o; o += up16(sizeof(double) * kW * (size_t)r);        // warp partials
-    cp = o; o += up16(sizeof(double) * 2 * (size_t)(r + kExtra));   // CTA partial [parity]
-    tot = o; o += up16(sizeof(double) * (r + kExtra));         // cluster totals
+    rb = o; o += up16(sizeof(double) * 2 * (size_t)G * (r + 1));   // received [parity][cta][r+1]
+    tot = o; o += up16(sizeof(double) * (r + 1));              // cluster totals (+ the error)
     xs = o; o += up16(sizeof(double) * kW * 4);                // warp extras
-    rdo = o; o += up16(sizeof(double) * 2);                    // read-out partials
+    rdo = o; o += up16(sizeof(double) * 4);                    // read-out partials
+    bar = o; o += up16(sizeof(uint64_t) * 2);                  // receive mbarriers [parity]
     total = o;
   }
 };
@@ -61,7 +65,7 @@ struct Lay {
 template <int NG>
 __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G, int nmax0, int nmax1) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const Lay L(A.r, nmax0, nmax1);
+  const Lay L(A.r, nmax0, nmax1, G);
   float* F0 = reinterpret_cast<float*>(smem + L.F0);
   float* F1 = reinterpret_cast<float*>(smem + L.F1);
   float* cw0 = reinterpret_cast<float*>(smem + L.c0);
@@ -70,15 +74,16 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
   float* vs = reinterpret_cast<float*>(smem + L.v);
   float* s32 = reinterpret_cast<float*>(smem + L.s32);
   double* wp = reinterpret_cast<double*>(smem + L.wp);
-  double* cp = reinterpret_cast<double*>(smem + L.cp);
+  double* rbuf = reinterpret_cast<double*>(smem + L.rb);
   double* tot = reinterpret_cast<double*>(smem + L.tot);
   double* xs = reinterpret_cast<double*>(smem + L.xs);
   double* rdo = reinterpret_cast<double*>(smem + L.rdo);
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(smem + L.bar);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int prob = blockIdx.x / G;
   const int cta = (int)cluster_ctarank();
-  const int r = A.r, R4 = r >> 2, RX = r + kExtra;
+  const int r = A.r, R4 = r >> 2, RX = r + 1;   // r-vector + the marginal error
   int64_t b0, e0, b1, e1;
   cta_rows(A.rows[0], G, cta, &b0, &e0);
   cta_rows(A.rows[1], G, cta, &b1, &e1);
@@ -97,9 +102,15 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
     for (int i = tid; i < n0; i += kT) cw0[i] = __ldg(a + i);
     for (int i = tid; i < n1; i += kT) cw1[i] = __ldg(b + i);
   }
-  __syncthreads();
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+  }
+  cluster_sync_all();   // every CTA's receive mbarriers are initialised before any push
 
-  double stErr = 0.0, stBrk = 0.0, stWb = 0.0, ferr = -1.0;
+  double stErr = 0.0, ferr = -1.0;
+  double brkT = 0.0, wbT = 0.0;   // this thread's breakdown / bad-weight counts (summed at the end)
   int final_t = -1, conv = 0;
   for (int p = 0; p < A.num_passes; ++p) {
     const int kind = pass_kind(p, A);
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
         acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
-    double errw = 0.0, brkw = 0.0, wbw = 0.0;
+    double errw = 0.0;
     int nb = 0;
     for (int rb = warp * kTR; rb < nr; rb += kW * kTR) {
       float4 fr[kTR][NG];
@@ -169,10 +180,10 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
           const float c = cw[row];
           const float w = c * rcp_approx(t);                    // w_j = c_j / t_j
           if ((lane & 3) == 0) {
-            if (bad_weight(c)) wbw += 1.0;
+            if (bad_weight(c)) wbT += 1.0;
             if (vold) errw += fabs((double)vold[row] * (double)t - (double)c);
             if (kOut) {
-              if (!(w > 0.f) || !isfinite(w)) brkw += 1.0;
+              if (!(w > 0.f) || !isfinite(w)) brkT += 1.0;
               outp[row] = w;
             }
           }
@@ -212,44 +223,44 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
         w4[3] = acc64[i][3];
       }
     }
-    errw = warp_sum_f64(errw);
-    brkw = warp_sum_f64(brkw);
-    wbw = warp_sum_f64(wbw);
-    if (lane == 0) {
-      xs[warp * 4 + 0] = errw;
-      xs[warp * 4 + 1] = brkw;
-      xs[warp * 4 + 2] = wbw;
-      xs[warp * 4 + 3] = 0.0;
+    const bool kErr = vold != nullptr;   // uniform: this pass evaluates the marginal error
+    if (kErr) {
+      errw = warp_sum_f64(errw);
+      if (lane == 0) xs[warp * 4] = errw;
     }
     __syncthreads();
-    // CTA partial (fixed warp order) into this pass's parity buffer
-    double* cpp = cp + (p & 1) * RX;
+    // CTA partial (fixed warp order), pushed into slot [p & 1][cta] of every CTA of the cluster
+    const uint32_t slot = smem_u32(rbuf + ((size_t)(p & 1) * G + cta) * RX);
+    const uint32_t mb = smem_u32(&rbar[p & 1]);
     for (int k = tid; k < RX; k += kT) {
       double x = 0.0;
       if (k < r) {
+        if (kAcc) {
 #pragma unroll
-        for (int w = 0; w < kW; ++w) x += wp[(size_t)w * r + k];
-      } else {
+          for (int w = 0; w < kW; ++w) x += wp[(size_t)w * r + k];
+        }
+      } else if (kErr) {
 #pragma unroll
-        for (int w = 0; w < kW; ++w) x += xs[w * 4 + (k - r)];
+        for (int w = 0; w < kW; ++w) x += xs[w * 4];
       }
-      cpp[k] = x;
+      for (int c = 0; c < G; ++c)
+        st_async_f64(mapa_shared(slot + 8u * (uint32_t)k, (uint32_t)c), x, mapa_shared(mb, (uint32_t)c));
     }
-    cluster_sync_all();   // every CTA's partial of pass p is complete and visible
+    if (tid == 0) mbar_arrive_expect_tx(&rbar[p & 1], (uint32_t)(G * RX * 8));
+    while (!mbar_try_wait_cluster(&rbar[p & 1], (uint32_t)((p >> 1) & 1))) {
+    }
     // cluster totals, CTA order 0..G-1 (the same bits in every CTA)
-    const uint32_t base = smem_u32(cpp);
+    const double* rp = rbuf + (size_t)(p & 1) * G * RX;
     for (int k = tid; k < RX; k += kT) {
       double x = 0.0;
-      for (int c = 0; c < G; ++c) x += ld_dsmem_f64(mapa_shared(base + 8u * (uint32_t)k, (uint32_t)c));
+      for (int c = 0; c < G; ++c) x += rp[(size_t)c * RX + k];
       tot[k] = x;
       if (k < r) s32[k] = (float)x;
     }
     __syncthreads();
-    // stopping test on pass p's extras (every thread: the same values, the same decision)
+    // stopping test on pass p's error (every thread: the same value, the same decision)
     {
-      const double e_err = tot[r], e_brk = tot[r + 1], e_wb = tot[r + 2];
-      stBrk += e_brk;
-      stWb += e_wb;
+      const double e_err = tot[r];
       if (kind == PK_V) {
         if (it >= 2) {
           stErr = e_err;
@@ -286,26 +297,28 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
   }
   la = warp_sum_f64(la);
   lb = warp_sum_f64(lb);
+  const double bk = warp_sum_f64(brkT), wb = warp_sum_f64(wbT);
+  __syncthreads();   // the last pass's readers of xs are done
   if (lane == 0) {
     xs[warp * 4 + 0] = la;
     xs[warp * 4 + 1] = lb;
+    xs[warp * 4 + 2] = bk;
+    xs[warp * 4 + 3] = wb;
   }
   __syncthreads();
-  if (tid == 0) {
-    double x = 0.0, y = 0.0;
-    for (int w = 0; w < kW; ++w) {
-      x += xs[w * 4 + 0];
-      y += xs[w * 4 + 1];
-    }
-    rdo[0] = x;
-    rdo[1] = y;
+  if (tid < 4) {
+    double x = 0.0;
+    for (int w = 0; w < kW; ++w) x += xs[w * 4 + tid];
+    rdo[tid] = x;
   }
   cluster_sync_all();
   if (cta == 0 && tid == 0) {
-    double x = 0.0, y = 0.0;
+    double x = 0.0, y = 0.0, stBrk = 0.0, stWb = 0.0;
     for (int c = 0; c < G; ++c) {
       x += ld_dsmem_f64(mapa_shared(smem_u32(rdo), (uint32_t)c));
       y += ld_dsmem_f64(mapa_shared(smem_u32(rdo + 1), (uint32_t)c));
+      stBrk += ld_dsmem_f64(mapa_shared(smem_u32(rdo + 2), (uint32_t)c));
+      stWb += ld_dsmem_f64(mapa_shared(smem_u32(rdo + 3), (uint32_t)c));
     }
     double* st = A.state + (int64_t)prob * kStateDoubles;
     st[ST_ITERS] = (double)final_t;
@@ -327,12 +340,12 @@ __global__ void __launch_bounds__(kT, 1) resident_kernel(const SinkArgs A, int G
 
 size_t resident_smem_bytes(int r, int64_t n, int64_t m, int G) {
   const int64_t n0 = (n + G - 1) / G, n1 = (m + G - 1) / G;
-  return res::Lay(r, (int)n0, (int)n1).total;
+  return res::Lay(r, (int)n0, (int)n1, G).total;
 }
 
 // smallest cluster that holds the factors (<= 227 KB per CTA), then more CTAs while half the
 // warps of every CTA still get a row batch (rows / G >= 4 warps x 8 rows).  Config 1 (500 rows,
-// r = 100), us per pass for G = 2 / 4 / 8: 3.29 / 2.42 / 2.08 (grid kernels: 6.36)
+// r = 100), us per pass for G = 4 / 8: 2.10 / 1.73 (grid kernels: 6.36)
 int resident_cluster(int r, int64_t n, int64_t m) {
   if (r > 512 || (r & 3)) return 0;
   const size_t cap = 227 * 1024;
@@ -344,13 +357,15 @@ int resident_cluster(int r, int64_t n, int64_t m) {
       break;
     }
   if (!G) return 0;
-  while (G < 8 && rows / (2 * G) >= (int64_t)(res::kW / 2) * res::kTR) G *= 2;
+  while (G < 8 && rows / (2 * G) >= (int64_t)(res::kW / 2) * res::kTR &&
+         resident_smem_bytes(r, n, m, 2 * G) <= cap)
+    G *= 2;
   return G;
 }
 
 cudaError_t launch_resident(const SinkArgs& a, int G, int batch, cudaStream_t s) {
   const int n0 = (int)((a.rows[0] + G - 1) / G), n1 = (int)((a.rows[1] + G - 1) / G);
-  const size_t dyn = res::Lay(a.r, n0, n1).total;
+  const size_t dyn = res::Lay(a.r, n0, n1, G).total;
   const int ng = (a.r / 4 + 31) / 32;
   void (*kern)(const SinkArgs, int, int, int) = nullptr;
   if (ng <= 1) kern = res::resident_kernel<1>;

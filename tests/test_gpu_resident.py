@@ -60,10 +60,11 @@ def _problem(n, m, d, r, eps, seed):
 
 
 @pytest.mark.parametrize("n,m,r,G", [(500, 500, 100, 8), (37, 53, 8, 1), (100, 97, 100, 2),
-                                     (300, 257, 100, 8), (1031, 997, 128, 8), (701, 803, 256, 8),
-                                     (200, 150, 512, 4), (1100, 1000, 196, 8), (1, 1, 4, 1),
-                                     (1300, 1300, 196, 0), (40000, 40000, 1000, 0),
-                                     (500, 500, 1024, 0), (20000, 20000, 100, 0)])
+                                     (150, 140, 100, 4), (300, 257, 100, 8), (1031, 997, 128, 8),
+                                     (600, 650, 256, 8), (200, 150, 512, 8), (1000, 900, 196, 8),
+                                     (1, 1, 4, 1), (701, 803, 256, 0), (1300, 1300, 196, 0),
+                                     (40000, 40000, 1000, 0), (500, 500, 1024, 0),
+                                     (20000, 20000, 100, 0)])
 def test_resident_plan(L, n, m, r, G):
     """The planner: the smallest cluster that holds both factors (<= 227 KB of shared memory per
     CTA), grown while half the warps keep a row batch; 0 (grid kernels) past r = 512 or 8 CTAs."""
@@ -88,11 +89,12 @@ def test_config1_full_resident_vs_oracle_and_grid(L, variant):
 @pytest.mark.parametrize("n,m,d,r", [
     (37, 53, 2, 8),        # G = 1, padded lanes
     (100, 97, 3, 100),     # G = 2
+    (150, 140, 2, 100),    # G = 4
     (300, 257, 2, 100),    # G = 8, 33-38 rows per CTA
     (1031, 997, 2, 128),   # G = 8, every lane one group
-    (701, 803, 3, 256),    # NG = 2
-    (200, 150, 2, 512),    # NG = 4, the largest r, G = 4
-    (1100, 1000, 2, 196),  # the factors need G = 8 (1.6 MB)
+    (600, 650, 3, 256),    # NG = 2
+    (200, 150, 2, 512),    # NG = 4, the largest r (needs G = 8)
+    (1000, 900, 2, 196),   # the factors need G = 8 (1.5 MB)
 ])
 def test_resident_shapes_vs_oracle(L, n, m, d, r):
     prob = _problem(n, m, d, r, 0.5, 17 + n)
