@@ -235,7 +235,7 @@ def _roofline(var, cfg_key, r, n_loc, m_loc, T, kmean_ms, batch=1, stream_rows=(
                 "frac": achieved / peak, "traffic": None,
                 "peak_source": "%d SMs x 128 B/clk x sm_max_mhz (%s)" % (resident, src),
                 "algorithmic_bytes_per_launch": alg_bytes, "cluster_ctas": resident,
-                "note": "one cluster barrier + DSMEM r-vector reduction per pass: latency-bound"}
+                "note": "per pass: st.async push of the CTA partials + one mbarrier wait: latency-bound"}
     if var == "implicit" and ns0 + ns1 > 0:
         entries = float(r) * (n_loc + T * (n_loc + m_loc))
         streamed = float(r) * (ns0 + T * (ns0 + ns1))

@@ -100,10 +100,11 @@ typedef struct lsk_solve_opts {
  * rep->rot is the value of the original problem (the offsets are folded in). */
 #define LSK_SOLVE_STABILIZE 1
 /* LSK_SOLVE_NO_RESIDENT: never use the resident small-problem kernel.  By default a
- * single-GPU, single-problem solve whose factors fit in the shared memory of one thread-block
- * cluster (<= 8 CTAs x 227 KB; r <= 512) keeps both factors on chip for the whole solve (the
- * implicit solver then materialises them once); this flag forces the persistent grid kernels
- * (same results within the parity tolerances; for tests and measurements). */
+ * single-GPU solve (one problem, or a batch: one cluster per problem) whose factors fit in the
+ * shared memory of one thread-block cluster (<= 8 CTAs x 227 KB; r <= 512) keeps both factors on
+ * chip for the whole solve (the implicit solvers then materialise them once); this flag forces
+ * the persistent grid kernels (same results within the parity tolerances; for tests and
+ * measurements). */
 #define LSK_SOLVE_NO_RESIDENT 2
 
 /* Report of one solve.  rot = W_hat of the returned (u, v);
@@ -379,7 +380,7 @@ lsk_status lsk_solve_plan(int64_t n, int64_t m, int32_t r, int32_t d, int32_t ba
                           int32_t variant, int32_t* gpp, int32_t* grid, int32_t* cluster);
 
 /* Diagnostic: the cluster size G (1, 2, 4 or 8 CTAs) of the resident small-problem kernel for a
- * single-GPU, single-problem solve of this shape (both factors held in the CTAs' shared memory
+ * single-GPU solve of this shape (per problem of a batch) (both factors held in the CTAs' shared memory
  * for the whole solve; DESIGN.md §6 K10), or 0 when the shape runs on the persistent grid
  * kernels (r > 512, or the factors exceed 8 x 227 KB).  LSK_SOLVE_NO_RESIDENT forces the grid
  * kernels; lsk_solve_plan describes those. */

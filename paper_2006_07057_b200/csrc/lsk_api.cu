@@ -416,7 +416,7 @@ static bool resident_allowed(const lsk_solve_opts* o) {
 
 static int resident_pick(const SinkArgs& A, int batch, const lsk_comm* comm,
                          const lsk_solve_opts* o) {
-  if (!resident_allowed(o) || batch != 1 || comm || A.emul || !A.F[0] || !A.F[1] || A.stab ||
+  if (!resident_allowed(o) || batch < 1 || comm || A.emul || !A.F[0] || !A.F[1] || A.stab ||
       A.nstream[0] + A.nstream[1] > 0)
     return 0;
   int G = resident_cluster(A.r, A.rows[0], A.rows[1]);
@@ -439,22 +439,22 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   A.tol = o->tol;
   A.want_err = (A.tol_mode || o->want_marginal_err) ? 1 : 0;
   A.num_passes = 2 * A.T + 1 + A.want_err;
-  if (const int G = resident_pick(A, batch, comm, o)) {
+  if (const int G = resident_pick(A, batch, comm, o)) {   // one cluster per problem
     Carve sz;
-    const size_t oState = sz.take(sizeof(double) * kStateDoubles);
+    const size_t oState = sz.take(sizeof(double) * kStateDoubles * batch);
     char* ws;
     LSK_TRY(get_ws(s, sz.off, &ws, 1));
     LSK_TRY(get_sticky(s, &A.sticky));
     A.state = reinterpret_cast<double*>(ws + oState);
-    LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles, s));
+    LSK_CU(cudaMemsetAsync(A.state, 0, sizeof(double) * kStateDoubles * batch, s));
     A.nranks = 1;
     A.rank = 0;
-    A.nprob = 1;
+    A.nprob = batch;
     A.gpp = G;
     A.pass_begin = 0;
     A.pass_end = A.num_passes;
-    LSK_CU(launch_resident(A, G, 1, s));
-    return collect_reports(A, 1, reps, false, s);
+    LSK_CU(launch_resident(A, G, batch, s));
+    return collect_reports(A, batch, reps, false, s);
   }
   SolveCfg c;
   LSK_TRY(plan_solve(A, impl, batch, o, &c, !comm && !A.emul));
@@ -1048,10 +1048,16 @@ lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, c
   Carve cv;
   const size_t oW = cv.take(sizeof(float) * p->d * p->r);
   const size_t oB = cv.take(sizeof(float) * p->r);
+  // small problems: every problem's factors materialised once (one FFMA feature-map launch per
+  // side over all batch x n rows: the anchors are shared) for the resident cluster kernel
+  const bool res = resident_allowed(o) && resident_cluster(p->r, n, m) > 0;
+  const size_t oD = res ? cv.take(sizeof(float) * p->r) : 0;
+  const size_t oF = res ? cv.take(sizeof(float) * (size_t)batch * (n + m) * p->r) : 0;
   LSK_TRY(get_ws(s, cv.off + solve_ws_bytes(n, m, batch), &ws));
   float* Wt = reinterpret_cast<float*>(ws + oW);
   float* b2 = reinterpret_cast<float*>(ws + oB);
-  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, nullptr, s));
+  float* bD = res ? reinterpret_cast<float*>(ws + oD) : nullptr;
+  LSK_CU(launch_anchor_prep(U, p->r, p->d, p->eps, p->q, p->log_scale, Wt, b2, bD, s));
   SinkArgs A{};
   A.X[0] = X; A.X[1] = Y;
   A.rows[0] = n; A.rows[1] = m;
@@ -1062,6 +1068,17 @@ lsk_status lsk_factored_sinkhorn_implicit_batched(const lsk_feature_params* p, c
   A.r = p->r; A.d = p->d; A.eps = p->eps;
   A.Wt = Wt; A.beta2 = b2;
   A.c2 = (float)(-2.0 * 1.4426950408889634074 / p->eps);
+  if (res) {
+    float* F0 = reinterpret_cast<float*>(ws + oF);
+    float* F1 = F0 + (size_t)batch * n * p->r;
+    LSK_CU(launch_feature_map(X, (int64_t)batch * n, p->d, U, Wt, b2, bD, p->r, p->eps, F0, s));
+    LSK_CU(launch_feature_map(Y, (int64_t)batch * m, p->d, U, Wt, b2, bD, p->r, p->eps, F1, s));
+    A.F[0] = F0;
+    A.F[1] = F1;
+    A.fstride[0] = n * p->r;   // factor rows per problem
+    A.fstride[1] = m * p->r;
+    return run_solve(A, false, batch, o, reps, nullptr, s);
+  }
   LSK_TRY(setup_fact(A, p->R, batch, s, ws, cv));
   return run_solve(A, true, batch, o, reps, nullptr, s);
 }

@@ -268,7 +268,18 @@ def test_cluster_mode_batched(L):
     u2 = torch.empty((B, n), dtype=torch.float32, device="cuda")
     v2 = torch.empty((B, n), dtype=torch.float32, device="cuda")
     reps2 = L.lsk_factored_sinkhorn_batched(Xi, Ze, a, b, 0.5, L.make_opts(T), u2, v2)
+    # the same batch on the grid kernels (these shapes otherwise run resident, one cluster per
+    # problem: test_gpu_resident.py)
+    u3 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    v3 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    reps3 = L.lsk_factored_sinkhorn_implicit_batched(p, U, X, Y, a, b,
+                                                     L.make_opts(T, resident=False), u3, v3)
+    u4 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    v4 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    reps4 = L.lsk_factored_sinkhorn_batched(Xi, Ze, a, b, 0.5, L.make_opts(T, resident=False), u4, v4)
     for q in range(B):
         ref = O.rot(bp["X"][q], bp["Y"][q], bp["a"][q], bp["b"][q], 0.5, 100, 11, T=T, R=R)
         _parity(u[q], v[q], reps[q].rot, ref)
         _parity(u2[q], v2[q], reps2[q].rot, ref)
+        _parity(u3[q], v3[q], reps3[q].rot, ref)
+        _parity(u4[q], v4[q], reps4[q].rot, ref)

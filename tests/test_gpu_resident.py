@@ -162,3 +162,52 @@ def test_resident_bad_weights_and_breakdown(L):
     with pytest.raises(L.LskError) as ei:
         _run(L, far, 10)
     assert ei.value.status in (EBREAKDOWN, EWEIGHTS)
+
+
+@pytest.mark.parametrize("B,n,m,r", [(7, 300, 257, 100), (64, 500, 500, 100)])
+def test_resident_batched(L, B, n, m, r):
+    """Batches of small problems: one cluster per problem (B x G CTAs; 64 x 8 = 512 CTAs is more
+    than one wave of clusters).  Both batched APIs against the oracle (a sample of the problems
+    for B = 64) and against the grid kernels for every problem."""
+    import torch
+    rng = np.random.default_rng(B)
+    d, eps, seed = 2, 0.5, 21
+    X = (rng.normal(0.0, 0.3, size=(B, n, d))).astype(np.float32)
+    Y = (rng.normal(0.2, 0.4, size=(B, m, d))).astype(np.float32)
+    a = rng.uniform(0.5, 1.5, size=(B, n)); a /= a.sum(1, keepdims=True)
+    b = rng.uniform(0.5, 1.5, size=(B, m)); b /= b.sum(1, keepdims=True)
+    a, b = a.astype(np.float32), b.astype(np.float32)
+    R = max(O.max_norm(X[q], Y[q]) for q in range(B))
+    Xd, Yd, ad, bd = _dev(X), _dev(Y), _dev(a), _dev(b)
+    p = L.lsk_feature_params_init(eps, d, r, R, seed)
+    U = torch.empty((r, d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    T = 50
+    out = {}
+    for res in (True, False):
+        u = torch.empty((B, n), dtype=torch.float32, device="cuda")
+        v = torch.empty((B, m), dtype=torch.float32, device="cuda")
+        reps = L.lsk_factored_sinkhorn_implicit_batched(p, U, Xd, Yd, ad, bd,
+                                                        L.make_opts(T, resident=res), u, v)
+        Xi = torch.empty((B, n, r), dtype=torch.float32, device="cuda")
+        Ze = torch.empty((B, m, r), dtype=torch.float32, device="cuda")
+        L.lsk_feature_map_batched(p, U, Xd, Xi)
+        L.lsk_feature_map_batched(p, U, Yd, Ze)
+        u2 = torch.empty((B, n), dtype=torch.float32, device="cuda")
+        v2 = torch.empty((B, m), dtype=torch.float32, device="cuda")
+        reps2 = L.lsk_factored_sinkhorn_batched(Xi, Ze, ad, bd, eps, L.make_opts(T, resident=res),
+                                                u2, v2)
+        out[res] = (u, v, reps, u2, v2, reps2)
+    sample = range(B) if B <= 8 else (0, 1, B // 2, B - 1)
+    for q in sample:
+        ref = O.rot(X[q], Y[q], a[q], b[q], eps, r, seed, T=T, R=R)
+        for (u, v, reps) in ((out[True][0], out[True][1], out[True][2]),
+                             (out[True][3], out[True][4], out[True][5])):
+            rot_err = abs(reps[q].rot - ref["rot"]) / abs(ref["rot"])
+            assert rot_err <= ROT_TOL, rot_err
+            assert _maxrel(u[q], ref["u"]) <= UV_TOL and _maxrel(v[q], ref["v"]) <= UV_TOL
+    for k in (0, 3):   # resident vs grid, every problem
+        for q in range(B):
+            g, h = out[False][k + 2][q].rot, out[True][k + 2][q].rot
+            assert abs(g - h) <= 2e-6 * abs(g), (q, g, h)
+            assert out[True][k + 2][q].iters == T
