@@ -3,7 +3,7 @@ protocol (L2 flush before every timed solve, CUDA events around the solve).  Nee
 build (LSK_LIB_PATH=scripts/variants/liblsk_tuning.so from `build.py --tuning`): the product
 library reads no environment.
 
-usage: python scripts/ab_env.py <config> <T or 0> NAME=VAR:VAL[,VAR:VAL] [NAME=...] ...
+usage: python scripts/ab_env.py <config> <T or 0> NAME=VAR:VAL[+VAR:VAL] [NAME=...] ...
 e.g.   python scripts/ab_env.py 2 0 off=LSK_STAGGER:0 on=LSK_STAGGER:1
 Prints median ms, us/pass and it/s per arm, and each arm's ROT / scalings against the first."""
 import os
@@ -22,7 +22,7 @@ T = int(sys.argv[2])
 arms = {}
 for spec in sys.argv[3:]:
     name, kv = spec.split("=", 1)
-    arms[name] = dict(x.split(":", 1) for x in kv.split(",") if x)
+    arms[name] = dict(x.split(":", 1) for x in kv.split("+") if x)
 cfg = synth.get_config(key, T=T) if T else synth.get_config(key)
 n = int(os.environ.get("AB_N", "0")) or None
 prob = synth.make_problem(cfg, n=n, m=n)
