@@ -93,6 +93,7 @@ __device__ __forceinline__ double fixed_max(const double* p, int nblk) {
 // scal[SC_M1], scal[SC_M2] = block maxima
 __global__ void __launch_bounds__(kThreads) lam_kernel(double tau, AccelVecs v) {
   __shared__ double red[kWarps];
+  if (v.ctl) tau = v.ctl[CT_TAU];   // graph-driven solve: this trial's tau
   const int side = blockIdx.y;
   const double* z = side ? v.zet2 : v.zet1;
   const double* e = side ? v.eta2 : v.eta1;
@@ -355,6 +356,12 @@ __global__ void __launch_bounds__(kThreads) stat3_kernel(AccelVecs v) {
 __global__ void __launch_bounds__(kThreads) accept_kernel(AccelVecs v, double a1, double Ak,
                                                           double Ak1) {
   __shared__ double red[kWarps];
+  if (v.ctl) {   // graph-driven solve: runs after every trial, moves only on acceptance
+    if (v.ctl[CT_ACC] == 0.0) return;   // uniform over the grid: no CTA takes a ticket
+    a1 = v.ctl[CT_A1];
+    Ak = v.ctl[CT_AKP];
+    Ak1 = v.ctl[CT_AK1];
+  }
   const double M1 = v.scal[SC_M1], M2 = v.scal[SC_M2], S1 = v.scal[SC_S1];
   const int blk = v.scal[SC_BLK] == 1.0 ? 1 : 2;
   const int side = blockIdx.y;
@@ -398,6 +405,86 @@ __global__ void __launch_bounds__(kThreads) normalise_kernel(const float* a, con
   if (threadIdx.x == 0) tot = s;
   __syncthreads();
   for (int64_t i = threadIdx.x; i < len; i += kThreads) out[i] = (double)x[i] / tot;
+}
+
+// ---- device-driven line search (graph-driven solve; the host loop's arithmetic, C24-C29) ----
+// iteration start: L_{k+1} = L_k / 2 (C24), trials re-armed
+__global__ void ls_begin_kernel(AccelVecs v, cudaGraphConditionalHandle trial) {
+  if (threadIdx.x != 0) return;
+  v.ctl[CT_L1] = v.ctl[CT_LK] / 2.0;
+  cudaGraphSetConditional(trial, 1u);
+}
+// trial start: a_{k+1} from L_{k+1} a_{k+1}^2 = A_k + a_{k+1}, tau = a_{k+1} / A_{k+1}
+__global__ void ls_prepare_kernel(AccelVecs v) {
+  if (threadIdx.x != 0) return;
+  double* c = v.ctl;
+  const double L1 = c[CT_L1], ak = c[CT_AK], Lk = c[CT_LK];
+  const double a1 = 1.0 / (2.0 * L1) + sqrt(1.0 / (4.0 * L1 * L1) + ak * ak * Lk / L1);
+  c[CT_A1] = a1;
+  c[CT_TAU] = 1.0 / (a1 * L1);
+  c[CT_TRIALS] += 1.0;
+  c[CT_ACC] = 0.0;
+}
+// accept (phi(eta_new) <= phi(lambda) - |grad|^2 / (2 L) + the C29 allowance) or double L
+__global__ void ls_decide_kernel(AccelVecs v, cudaGraphConditionalHandle trial,
+                                 cudaGraphConditionalHandle iter) {
+  if (threadIdx.x != 0) return;
+  const double* sc = v.scal;
+  double* c = v.ctl;
+  const double M1 = sc[SC_M1], M2 = sc[SC_M2], S1 = sc[SC_S1], S2 = sc[SC_S2];
+  const double la = sc[SC_LA], lb = sc[SC_LB], n1 = sc[SC_N1], n2 = sc[SC_N2];
+  if (sc[SC_BAD] > 0.0 || !(S1 > 0.0) || !isfinite(S1) || !(S2 > 0.0)) {
+    c[CT_ERR] = 1.0;   // breakdown: both loops end
+    cudaGraphSetConditional(trial, 0u);
+    cudaGraphSetConditional(iter, 0u);
+    return;
+  }
+  const int blk = sc[SC_BLK] == 1.0 ? 1 : 2;   // argmax, ties -> 1 (C27)
+  const double phi_lam = M1 + M2 + log(blk == 1 ? S1 : S2) - la - lb;
+  const double phi_new = log(sc[SC_E]) - (blk == 1 ? sc[SC_EW] + lb : la + sc[SC_EW]);
+  const double L1 = c[CT_L1], a1 = c[CT_A1];
+  if (phi_new <= phi_lam - (n1 + n2) / (2.0 * L1) + 1e-13 * fmax(1.0, fabs(phi_lam))) {
+    c[CT_ACC] = 1.0;
+    c[CT_AKP] = c[CT_LK] * c[CT_AK] * c[CT_AK];   // A_k = L_k a_k^2
+    c[CT_AK1] = L1 * a1 * a1;                     // A_{k+1}
+    c[CT_AK] = a1;
+    c[CT_LK] = L1;
+    c[CT_PHI] = phi_new;
+    c[CT_BLK] = (double)blk;
+    cudaGraphSetConditional(trial, 0u);
+  } else {
+    c[CT_L1] = 2.0 * L1;
+    if (!(2.0 * L1 < 1e300)) {
+      c[CT_ERR] = 2.0;   // the line search diverged
+      cudaGraphSetConditional(trial, 0u);
+      cudaGraphSetConditional(iter, 0u);
+    }
+  }
+}
+// iteration end: traces, the iteration count and the stopping test (tol on the averaged plan)
+__global__ void ls_end_kernel(AccelVecs v, cudaGraphConditionalHandle iter, double eps,
+                              int max_iters, double tol, double* Ftr, double* Ltr, int* Btr) {
+  if (threadIdx.x != 0) return;
+  double* c = v.ctl;
+  if (c[CT_ERR] != 0.0) {
+    cudaGraphSetConditional(iter, 0u);
+    return;
+  }
+  const int it = (int)c[CT_IT];
+  const double F = -eps * c[CT_PHI];
+  c[CT_F] = F;
+  if (Ftr) Ftr[it] = F;
+  if (Ltr) Ltr[it] = c[CT_LK];
+  if (Btr) Btr[it] = (int)c[CT_BLK];
+  c[CT_IT] = (double)(it + 1);
+  const double perr = v.scal[SC_PERR];
+  c[CT_PERR] = perr;
+  bool stop = it + 1 >= max_iters;
+  if (tol > 0.0 && perr < tol) {
+    c[CT_CONV] = 1.0;
+    stop = true;
+  }
+  cudaGraphSetConditional(iter, stop ? 0u : 1u);
 }
 
 }  // namespace accel
@@ -451,6 +538,94 @@ cudaError_t launch_accel_pass(const float* F, int64_t rows, int r, const double*
   if (r <= 1024) return pass_nv<8>(F, rows, r, s_in, lam, Mp, t_out, part, s);
   if (r <= 2048) return pass_nv<16>(F, rows, r, s_in, lam, Mp, t_out, part, s);
   return cudaErrorInvalidValue;
+}
+
+static cudaError_t add_kernel_node(cudaGraph_t g, const cudaGraphNode_t* dep, size_t ndep,
+                                   void* func, void** args, cudaGraphNode_t* out) {
+  cudaKernelNodeParams kp = {};
+  kp.func = func;
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  return cudaGraphAddKernelNode(out, g, dep, ndep, &kp);
+}
+
+cudaError_t accel_solve_graph(const AccelVecs& v, const float* Xi, int64_t n, const float* Zeta,
+                              int64_t m, int r, double* partA, double* partB, double eps,
+                              int max_iters, double tol, double* Ftr, double* Ltr, int* Btr,
+                              cudaStream_t s) {
+  const int Gp = accel_pass_grid();
+  cudaGraph_t g = nullptr, body1, body2;
+  cudaGraphExec_t ge = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaError_t e;
+#define GT(x)                \
+  do {                       \
+    e = (x);                 \
+    if (e != cudaSuccess) goto done; \
+  } while (0)
+  {
+    GT(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hIter, hTrial;
+    GT(cudaGraphConditionalHandleCreate(&hIter, g, 1u, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hIter;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t nIter;
+    GT(cudaGraphAddNode(&nIter, g, nullptr, 0, &cp));
+    body1 = cp.conditional.phGraph_out[0];
+    // iteration body: begin -> while(trial) -> end
+    GT(cudaGraphConditionalHandleCreate(&hTrial, body1, 1u, cudaGraphCondAssignDefault));
+    AccelVecs va = v;
+    cudaGraphNode_t nBegin, nTrial, nEnd;
+    {
+      void* args[] = {&va, &hTrial};
+      GT(add_kernel_node(body1, nullptr, 0, (void*)accel::ls_begin_kernel, args, &nBegin));
+    }
+    cudaGraphNodeParams tp = {};
+    tp.type = cudaGraphNodeTypeConditional;
+    tp.conditional.handle = hTrial;
+    tp.conditional.type = cudaGraphCondTypeWhile;
+    tp.conditional.size = 1;
+    GT(cudaGraphAddNode(&nTrial, body1, &nBegin, 1, &tp));
+    body2 = tp.conditional.phGraph_out[0];
+    {
+      double eps_ = eps, tol_ = tol;
+      int mi = max_iters;
+      void* args[] = {&va, &hIter, &eps_, &mi, &tol_, &Ftr, &Ltr, &Btr};
+      GT(add_kernel_node(body1, &nTrial, 1, (void*)accel::ls_end_kernel, args, &nEnd));
+    }
+    // trial body, captured from the same launchers the host-driven loop uses
+    GT(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    GT(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    accel::ls_prepare_kernel<<<1, 32, 0, cs>>>(va);
+    launch_accel_lambda(0.0, va, cs);
+    launch_accel_pass(Zeta, m, r, nullptr, va.lam2, va.scal + SC_M2, nullptr, partA, cs);
+    launch_accel_pass(Xi, n, r, partA + (size_t)Gp * r, va.lam1, va.scal + SC_M1, va.t1, partB, cs);
+    launch_accel_pass(Zeta, m, r, partB + (size_t)Gp * r, nullptr, nullptr, va.t2, nullptr, cs);
+    launch_accel_stats(1, va, 0, 0, 0, cs);
+    launch_accel_stats(2, va, 0, 0, 0, cs);
+    launch_accel_stats(3, va, 0, 0, 0, cs);
+    accel::ls_decide_kernel<<<1, 32, 0, cs>>>(va, hTrial, hIter);
+    launch_accel_stats(4, va, 0, 0, 0, cs);
+    {
+      cudaGraph_t cap = nullptr;
+      GT(cudaStreamEndCapture(cs, &cap));
+    }
+    GT(cudaGraphInstantiate(&ge, g, 0));
+    GT(cudaGraphLaunch(ge, s));
+    count_launch(2);
+  }
+done:
+#undef GT
+  if (ge) cudaGraphExecDestroy(ge);   // destruction waits for nothing: the launch is enqueued
+  if (g) cudaGraphDestroy(g);
+  if (cs) cudaStreamDestroy(cs);
+  return e;
 }
 
 cudaError_t launch_accel_stats(int phase, const AccelVecs& v, double a1, double Ak, double Ak1,

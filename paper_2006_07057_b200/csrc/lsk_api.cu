@@ -1313,6 +1313,9 @@ lsk_status lsk_accelerated_sinkhorn(const float* Xi, int64_t n, const float* Zet
   const size_t o_en = cv.take(8 * mx), o_pt = cv.take(8 * 6 * G), o_sc = cv.take(8 * 32),
                o_tk = cv.take(256);
   const size_t o_pa = cv.take(8 * (size_t)(Gp + 1) * r), o_pb = cv.take(8 * (size_t)(Gp + 1) * r);
+  const size_t o_ct = cv.take(8 * CT_COUNT);
+  const size_t o_tf = cv.take(8 * (size_t)o->max_iters), o_tl = cv.take(8 * (size_t)o->max_iters),
+               o_tb = cv.take(4 * (size_t)o->max_iters);
   char* ws;
   LSK_TRY(get_ws(s, cv.off, &ws));
   auto D = [&](size_t off) { return reinterpret_cast<double*>(ws + off); };
@@ -1339,6 +1342,51 @@ lsk_status lsk_accelerated_sinkhorn(const float* Xi, int64_t n, const float* Zet
   double ak = 0.0, Lk = o->L0, F = 0.0, plan_err = -1.0;
   int it = 0, trials = 0;
   bool converged = false;
+  // The whole solve as one CUDA graph (device-side line search, DESIGN.md §6 K7): one
+  // synchronisation per solve instead of one per trial; the host-driven loop below remains
+  // the fallback when the graph cannot be built (tuning builds: LSK_ACCEL_HOST=1 forces it).
+  const char* force_host = tuning_env("LSK_ACCEL_HOST");
+  if (!(force_host && atoi(force_host) == 1)) {
+    double ct[CT_COUNT] = {};
+    ct[CT_LK] = o->L0;
+    double* ctl = D(o_ct);
+    LSK_CU(cudaMemcpyAsync(ctl, ct, sizeof(ct), cudaMemcpyHostToDevice, s));
+    v.ctl = ctl;
+    double* dF = D(o_tf);
+    double* dL = D(o_tl);
+    int* dB = reinterpret_cast<int*>(ws + o_tb);
+    const cudaError_t ge = accel_solve_graph(v, Xi, n, Zeta, m, r, partA, partB, eps, o->max_iters,
+                                             o->tol, dF, dL, dB, s);
+    if (ge == cudaSuccess) {
+      LSK_CU(cudaMemcpyAsync(ct, ctl, sizeof(ct), cudaMemcpyDeviceToHost, s));
+      LSK_CU(cudaStreamSynchronize(s));
+      it = (int)ct[CT_IT];
+      if (it > 0) {
+        if (F_trace) LSK_CU(cudaMemcpy(F_trace, dF, 8 * (size_t)it, cudaMemcpyDeviceToHost));
+        if (L_trace) LSK_CU(cudaMemcpy(L_trace, dL, 8 * (size_t)it, cudaMemcpyDeviceToHost));
+        if (blk_trace) LSK_CU(cudaMemcpy(blk_trace, dB, 4 * (size_t)it, cudaMemcpyDeviceToHost));
+      }
+      if (ct[CT_ERR] == 1.0)
+        return fail(LSK_EBREAKDOWN, "zero or non-finite K e^lambda during the accelerated solve");
+      if (ct[CT_ERR] != 0.0) return fail(LSK_EBREAKDOWN, "line search diverged");
+      if (rep) {
+        rep->iters = it;
+        rep->trials = (int32_t)ct[CT_TRIALS];
+        rep->converged = ct[CT_CONV] != 0.0 ? 1 : 0;
+        rep->reserved = 0;
+        rep->F = ct[CT_F];
+        rep->L = ct[CT_LK];
+        rep->plan_err = ct[CT_PERR];
+      }
+      if (o->tol > 0.0 && ct[CT_CONV] == 0.0) {
+        g_err = "tolerance not reached within max_iters";
+        return LSK_NOT_CONVERGED;
+      }
+      return LSK_OK;
+    }
+    (void)cudaGetLastError();   // the graph was not launched: the host-driven loop
+    v.ctl = nullptr;
+  }
   for (; it < o->max_iters;) {
     double L1 = Lk / 2.0;   // C24: one halving, then doubling on rejection
     double phi_new = 0.0;

@@ -202,7 +202,23 @@ struct AccelVecs {
   double *part;                          // per-CTA partials (>= 6 * accel_grid())
   double *scal;                          // [SC_COUNT]
   unsigned int* ticket;                  // last-CTA counter (zero between launches)
+  double* ctl;                           // device line-search state [CT_COUNT] (graph-driven
+                                         // solve; NULL: the host drives the line search)
 };
+// device line-search state of the graph-driven accelerated solve (lsk_accel.cu)
+enum AccelCtl {
+  CT_AK = 0, CT_LK, CT_L1, CT_A1, CT_TAU, CT_IT, CT_TRIALS, CT_F, CT_ERR, CT_CONV, CT_PHI,
+  CT_ACC, CT_AKP, CT_AK1, CT_BLK, CT_PERR, CT_COUNT
+};
+// The whole accelerated solve as ONE CUDA graph launch: a while-node over iterations whose
+// body holds a while-node over line-search trials; the accept / double-L decision, the
+// iteration count and the tolerance test run on the device (cudaGraphSetConditional), so the
+// host synchronises once per solve instead of once per trial.  v.ctl must be initialised
+// (CT_AK = 0, CT_LK = L0, the rest 0).  Traces (nullable) are device arrays of max_iters.
+cudaError_t accel_solve_graph(const AccelVecs& v, const float* Xi, int64_t n, const float* Zeta,
+                              int64_t m, int r, double* partA, double* partB, double eps,
+                              int max_iters, double tol, double* Ftr, double* Ltr, int* Btr,
+                              cudaStream_t s);
 int accel_grid();
 int accel_pass_grid();
 cudaError_t launch_accel_normalise(const float* a, const float* b, const AccelVecs& v,
