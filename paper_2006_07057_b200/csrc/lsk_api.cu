@@ -402,6 +402,7 @@ static lsk_status plan_solve(SinkArgs& A, bool impl, int batch, const lsk_solve_
 }
 
 constexpr int kPreDefault = 2;
+constexpr int kPingPongDefault = 1;
 
 static lsk_status collect_reports(const SinkArgs& A, int batch, lsk_report* reps, bool nccl_rot,
                                   cudaStream_t s);
@@ -463,6 +464,8 @@ static lsk_status run_solve(SinkArgs A, bool impl, int batch, const lsk_solve_op
   // only: the cluster boundary has no wait to hide it in)
   A.pre = A.cx ? 0 : kPreDefault;
   if (const char* e = tuning_env("LSK_PRE")) A.pre = std::max(0, std::min(2, atoi(e)));
+  A.pingpong = kPingPongDefault;   // implicit two-team kernel: alternating generations (§6 K5)
+  if (const char* e = tuning_env("LSK_PP")) A.pingpong = atoi(e) != 0;
   if (impl && A.d > 8) return fail(LSK_EDIM, "implicit variant supports d <= 8");
   const bool p2p = !A.emul && comm && comm->p2p && batch == 1 && A.r + kExtra + 2 <= comm->xrs &&
                    !(getenv("LSK_P2P") && atoi(getenv("LSK_P2P")) == 0);

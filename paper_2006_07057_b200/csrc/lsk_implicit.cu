@@ -568,6 +568,8 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       constexpr bool kAcc = KIND != PK_ERR;
       constexpr bool kOut = KIND == PK_U || KIND == PK_V;
       auto issue = [&](int t) { issue_tile(feed, gt0, t); };
+      constexpr bool kPP = !PIPE && SW == 0 && TEAMS == 2;
+      const bool pp = kPP && A.pingpong != 0;
       if (twarp == 0) {
         if (!prefetched) {
 #pragma unroll
@@ -583,13 +585,24 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
 
       // generate tile t's features into fr and publish its row-dot partials
       // GEN = false: fr already holds the tile (generated at the previous pass boundary)
+      // Ping-pong (two teams): the teams' feature generations alternate — team 0 generates
+      // tile t after team 1's tile t-1 (barrier 10), team 1 tile t after team 0's tile t
+      // (barrier 11) — so one team's exchange and accumulation (shuffle / shared-memory work in
+      // the MIO queue) run under the other team's ex2 instead of both teams generating at once
+      // and then both leaving the MUFU idle.
       auto compute = [&](int t, float2 (&fr)[TR][NV][2], auto gen_tag) {
         if (twarp == 0) issue(t + kAhead);
         const uint32_t gi = gt0 + (uint32_t)t;
         const float* sl = tslots + (gi % kRing) * SLOT;
         if constexpr (PIPE) mbar_wait(&S.full[team][gi % kRing], (gi / kRing) & 1u);
+        if constexpr (kPP) {
+          if (pp && (team == 1 || t > 0)) named_bar(team == 0 ? 10u : 11u, 2 * TS);
+        }
         if constexpr (decltype(gen_tag)::value) gen_features(sl, fr);
         else stash_load(fr);
+        if constexpr (kPP) {
+          if (pp) named_arrive(team == 0 ? 11u : 10u, 2 * TS);
+        }
         const int rb = (int)(gi % 3u);
         if constexpr (kDot) {
           float pr[TR];
@@ -711,6 +724,13 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
         for (int t = t0; t < ntiles; ++t) {
           compute(t, frA, std::true_type{});
           finish(t, frA);
+        }
+        if constexpr (kPP) {   // balance the ping-pong barriers when the teams' tile counts differ
+          if (pp) {
+            const int nt = (nrows + TR - 1) / TR, n0 = (nt + 1) / 2, n1 = nt / 2;
+            if (team == 1 && n1 < n0) named_bar(11u, 2 * TS);
+            if (team == 0 && n1 == n0 && n0 > 0) named_bar(10u, 2 * TS);
+          }
         }
       }
     };

@@ -96,6 +96,7 @@ struct SinkArgs {
   int emul;                // 1: the nprob problems of this launch are the nranks ranks of ONE
                            // row-sharded solve (rank = problem index; xbox[] all on this GPU):
                            // the cross-GPU exchange emulated inside one cooperative launch
+  int pingpong;            // implicit kernel, two teams: the teams' feature generations alternate
   int pre;                 // implicit team kernel: generate the next pass's first feature tile
                            // at the pass boundary (0 off, 1 after R2, 2 inside the barrier)
 };

@@ -87,6 +87,9 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---- gpu-scope release / acquire on a global counter -----------------------------------
 __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
