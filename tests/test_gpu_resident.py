@@ -211,3 +211,20 @@ def test_resident_batched(L, B, n, m, r):
             g, h = out[False][k + 2][q].rot, out[True][k + 2][q].rot
             assert abs(g - h) <= 2e-6 * abs(g), (q, g, h)
             assert out[True][k + 2][q].iters == T
+
+
+@pytest.mark.parametrize("n,m", [(16, 7), (17, 40), (40, 90), (300, 129), (1, 33)])
+def test_two_team_pingpong_tile_counts(L, n, m):
+    """The implicit grid kernel's two-team configuration (32 < r/4 <= 256, d <= 3) with its
+    ping-pong hand-over between the teams (DESIGN.md §6 K5): shapes whose CTAs hold 0, 1, 2 or 3
+    tiles of each side, i.e. equal and unequal team tile counts and a team with no tile, so the
+    end-of-pass balancing of the hand-over barriers is exercised on both sides.  Forced onto the
+    grid kernels (these shapes would otherwise run resident) and compared with the oracle."""
+    prob = _problem(n, m, 2, 256, 0.5, 5 + n + m)
+    T = 30
+    ref = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], prob["eps"], 256, prob["seed"], T=T)
+    _check(_run(L, prob, T, variant="implicit", resident=False), ref)
+    res_t = _run(L, prob, 400, variant="implicit", tol=1e-6, resident=False)
+    ref_t = O.rot(prob["X"], prob["Y"], prob["a"], prob["b"], prob["eps"], 256, prob["seed"], tol=1e-6)
+    assert res_t["report"]["converged"] == 1
+    assert abs(res_t["report"]["iters"] - ref_t["iters"]) <= 1
