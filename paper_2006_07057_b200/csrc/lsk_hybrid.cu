@@ -275,9 +275,8 @@ __global__ void __launch_bounds__(NT, 1) hybrid_kernel(const SinkArgs A) {
         if (tid == 0) {
           const int q = p - 1;
           const int qk = pass_kind(q, A);
-          const double e_err = sv_load(sv_of(A, 0, q) + r, false);
-          const double e_brk = sv_load(sv_of(A, 0, q) + r + 1, false);
-          const double e_wb = sv_load(sv_of(A, 0, q) + r + 2, false);
+          double e_err, e_brk, e_wb;
+          sv_load_extras(sv_of(A, 0, q) + r, false, e_err, e_brk, e_wb);
           S.st[1] += e_brk;
           S.st[3] += e_wb;
           if (qk == PK_V) {
@@ -310,8 +309,8 @@ __global__ void __launch_bounds__(NT, 1) hybrid_kernel(const SinkArgs A) {
         for (int gg = tid; gg < NV * TS; gg += NT) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
           if (gg < R4) {
-            const double2 lo = sv_load2(sv_of(A, 0, p - 1) + 4 * gg, false);
-            const double2 hi = sv_load2(sv_of(A, 0, p - 1) + 4 * gg + 2, false);
+            double2 lo, hi;
+            sv_load4(sv_of(A, 0, p - 1) + 4 * gg, false, lo, hi);
             v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
           }
           s_sm[gg] = v;

@@ -479,9 +479,7 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
           e_brk = x[1];
           e_wb = x[2];
         } else if (A.gpp > 1) {
-          e_err = sv_load(sv_of(A, prob, q) + r, multi);
-          e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
-          e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
+          sv_load_extras(sv_of(A, prob, q) + r, multi, e_err, e_brk, e_wb);
         } else {
           e_err = S.ext[0];
           e_brk = S.ext[1];
@@ -527,8 +525,8 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
             cx_total4(cxtot, A.gpp, gg, x);
             v = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
           } else if (A.gpp > 1) {
-            const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * gg, multi);
-            const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * gg + 2, multi);
+            double2 lo, hi;
+            sv_load4(sv_of(A, prob, p - 1) + 4 * gg, multi, lo, hi);
             v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
           } else {   // gpp == 1: the combined accumulator sits in team 0's slots
             const int t0 = gg % TS, j = gg / TS;
@@ -781,33 +779,29 @@ __global__ void __launch_bounds__(TS * TEAMS + 32 * SW, 1) implicit_kernel(const
       S.xs[1][NW - 1 - team] = e1;
       S.xs[2][NW - 1 - team] = e2;
     }
-    named_bar(1, NT);
-    if (!strm && ttid == 0) {
-      e0 = S.xs[0][NW - 1 - team];
-      e1 = S.xs[1][NW - 1 - team];
-      e2 = S.xs[2][NW - 1 - team];
-    }
-    named_bar(1, NT);
-    if constexpr (TEAMS > 1) {
-      if (!strm && team > 0 && ttid == 0) {
-        S.xs[0][team] = e0;
-        S.xs[1][team] = e1;
-        S.xs[2][team] = e2;
+    named_bar(1, NT);   // every team's accumulators and extras are in shared memory
+    if (!strm && tid == 0) {   // the extras, fixed order: team 0 + team 1 + ... (deterministic)
+      e0 = S.xs[0][NW - 1];
+      e1 = S.xs[1][NW - 1];
+      e2 = S.xs[2][NW - 1];
+#pragma unroll
+      for (int tm = 1; tm < TEAMS; ++tm) {
+        e0 += S.xs[0][NW - 1 - tm];
+        e1 += S.xs[1][NW - 1 - tm];
+        e2 += S.xs[2][NW - 1 - tm];
       }
-      named_bar(1, NT);
+    }
+    if constexpr (TEAMS > 1) {
       if (team == 0) {   // fixed order: team 0 + team 1 + ... (deterministic)
 #pragma unroll
         for (int tm = 1; tm < TEAMS; ++tm) {
 #pragma unroll
           for (int e = 0; e < NV * 4; ++e) acc_s[e][ttid] += acc_s[e][ttid + tm * TS];
-          if (ttid == 0) {
-            e0 += S.xs[0][tm];
-            e1 += S.xs[1][tm];
-            e2 += S.xs[2][tm];
-          }
         }
       }
-      named_bar(1, NT);
+      // R1 (gpp > 1, no cluster) stores each team-0 thread's own combined columns and starts
+      // with a CTA barrier of its own; the other boundary forms read other threads' columns
+      if (A.gpp == 1 || A.cx || SW > 0) named_bar(1, NT);
     }
     if constexpr (SW > 0) {   // then the stream warps' partials, warp 0, 1, ... (fixed order)
       if (team == 0) {

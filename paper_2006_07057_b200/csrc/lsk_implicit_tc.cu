@@ -285,9 +285,8 @@ __global__ void __launch_bounds__(NT, 1) itc_kernel(const SinkArgs A) {
       if (tid == 0) {
         const int q = p - 1;
         const int qk = pass_kind(q, A);
-        const double e_err = sv_load(sv_of(A, 0, q) + r, false);
-        const double e_brk = sv_load(sv_of(A, 0, q) + r + 1, false);
-        const double e_wb = sv_load(sv_of(A, 0, q) + r + 2, false);
+        double e_err, e_brk, e_wb;
+        sv_load_extras(sv_of(A, 0, q) + r, false, e_err, e_brk, e_wb);
         S.st[1] += e_brk;
         S.st[3] += e_wb;
         if (qk == PK_V) {

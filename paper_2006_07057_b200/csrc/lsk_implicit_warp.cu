@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1) implicit_warp_kernel(const Sink
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (g < R4) {
           if (A.gpp > 1) {
-            const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g, multi);
-            const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g + 2, multi);
+            double2 lo, hi;
+            sv_load4(sv_of(A, prob, p - 1) + 4 * g, multi, lo, hi);
             v = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
           } else {   // element (4 j + q) * 32 + l holds column 4 (l + 32 j) + q
             const int l = g & 31, j = g >> 5;

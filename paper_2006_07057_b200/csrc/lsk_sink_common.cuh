@@ -98,6 +98,51 @@ __device__ __forceinline__ double2 sv_load2(const double* p, bool multi) {
   return make_double2(__longlong_as_double((long long)b0), __longlong_as_double((long long)b1));
 }
 
+// four consecutive values (a float4 column group) in one poll: one L2 round trip instead of
+// the two of back-to-back sv_load2 calls
+__device__ __forceinline__ void sv_load4(const double* p, bool multi, double2& lo, double2& hi) {
+  if (multi) {
+    lo = __ldcg(reinterpret_cast<const double2*>(p));
+    hi = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+    return;
+  }
+  unsigned long long b0, b1, b2, b3;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%4];\n\t"
+                 "ld.relaxed.gpu.global.v2.b64 {%2, %3}, [%5];"
+                 : "=l"(b0), "=l"(b1), "=l"(b2), "=l"(b3) : "l"(p), "l"(p + 2) : "memory");
+    if (b0 != kSvSentinel && b1 != kSvSentinel && b2 != kSvSentinel && b3 != kSvSentinel) break;
+    __nanosleep(100);
+  }
+  lo = make_double2(__longlong_as_double((long long)b0), __longlong_as_double((long long)b1));
+  hi = make_double2(__longlong_as_double((long long)b2), __longlong_as_double((long long)b3));
+}
+
+// the pass's extras (block r/4: err, breakdowns, bad weights, 0) in one poll: both 16-byte
+// loads are issued before either is tested, so the three values cost one L2 round trip
+// (three sequential sv_load calls cost three, on the path every CTA waits on)
+__device__ __forceinline__ void sv_load_extras(const double* p, bool multi, double& e_err,
+                                               double& e_brk, double& e_wb) {
+  if (multi) {
+    const double2 lo = __ldcg(reinterpret_cast<const double2*>(p));
+    e_err = lo.x;
+    e_brk = lo.y;
+    e_wb = __ldcg(p + 2);
+    return;
+  }
+  unsigned long long b0, b1, b2, b3;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%4];\n\t"
+                 "ld.relaxed.gpu.global.v2.b64 {%2, %3}, [%5];"
+                 : "=l"(b0), "=l"(b1), "=l"(b2), "=l"(b3) : "l"(p), "l"(p + 2) : "memory");
+    if (b0 != kSvSentinel && b1 != kSvSentinel && b2 != kSvSentinel && b3 != kSvSentinel) break;
+    __nanosleep(100);
+  }
+  e_err = __longlong_as_double((long long)b0);
+  e_brk = __longlong_as_double((long long)b1);
+  e_wb = __longlong_as_double((long long)b2);
+}
+
 // ---- cross-GPU exchange over NVLink peer memory (one persistent launch per GPU) -----------
 // The owner of column k on every rank (same CTA partition on every rank) adds the ranks' local
 // totals in rank order: it stores its own total into slot [par][my rank][k] of EVERY rank's

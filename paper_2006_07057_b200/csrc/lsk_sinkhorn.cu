@@ -229,9 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         e_brk = x[1];
         e_wb = x[2];
       } else if (A.gpp > 1) {
-        e_err = sv_load(sv_of(A, prob, q) + r, multi);
-        e_brk = sv_load(sv_of(A, prob, q) + r + 1, multi);
-        e_wb = sv_load(sv_of(A, prob, q) + r + 2, multi);
+        sv_load_extras(sv_of(A, prob, q) + r, multi, e_err, e_brk, e_wb);
       } else {
         e_err = S.ext[0];
         e_brk = S.ext[1];
@@ -293,8 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1) sinkhorn_kernel(const SinkArgs A)
         for (int j = 0; j < NV; ++j) {
           if (gv[j]) {
             if constexpr (CW == 4) {
-              const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j], multi);
-              const double2 hi = sv_load2(sv_of(A, prob, p - 1) + 4 * g[j] + 2, multi);
+              double2 lo, hi;
+              sv_load4(sv_of(A, prob, p - 1) + 4 * g[j], multi, lo, hi);
               s[j] = make_float4((float)lo.x, (float)lo.y, (float)hi.x, (float)hi.y);
             } else {
               const double2 lo = sv_load2(sv_of(A, prob, p - 1) + 2 * g[j], multi);
