@@ -47,6 +47,7 @@ def _check_parity(res, ref, rot_tol=ROT_TOL, uv_tol=UV_TOL):
     rot_err = abs(res["rot"] - ref["rot"]) / abs(ref["rot"])
     u_err = _maxrel(res["u"], ref["u"])
     v_err = _maxrel(res["v"], ref["v"])
+    print("parity: rot %.3e u %.3e v %.3e" % (rot_err, u_err, v_err))   # shown with pytest -s
     assert rot_err <= rot_tol and u_err <= uv_tol and v_err <= uv_tol, (rot_err, u_err, v_err)
     return rot_err, u_err, v_err
 
