@@ -129,39 +129,66 @@ cudaError_t launch_anchor_prep(const float* U, int r, int d, double eps, double 
 
 // ---------------------------------------------------------------- a3: feature map --------
 // d <= 16, direct form: e2 = betaD_k + c2 * sum_c (x_ic - U_kc)^2, xi = 2^e2.
-// Block = 256 threads x 32 rows; thread t owns float4 column groups t, t+256, ...
+// Block = 256 threads x RB rows (32 for d < 8, where the kernel is write-bound; 64 for d >= 8,
+// where the anchor loads per column group are amortised over more rows); thread t owns float4
+// column groups t, t+256, ...  The next row's coordinates are read from shared memory while
+// the current row is computed (one row ahead, in registers).
+template <int D> struct DirectRows { static constexpr int value = D >= 8 ? 64 : 32; };
+
 template <int D>
 __global__ void __launch_bounds__(256) feature_map_direct_kernel(
     const float* __restrict__ X, int64_t n, const float* __restrict__ U,
     const float* __restrict__ betaD, int r, float c2, float* __restrict__ Xi) {
-  constexpr int RB = 32;
-  __shared__ float xs[RB][D];
+  constexpr int RB = DirectRows<D>::value;
+  __shared__ __align__(16) float xs[RB + 1][D];   // row RB: zero pad read by the look-ahead
   const int64_t row0 = (int64_t)blockIdx.x * RB;
   const int rows = (int)min((int64_t)RB, n - row0);
-  for (int i = threadIdx.x; i < rows * D; i += blockDim.x) xs[i / D][i % D] = X[row0 * D + i];
+  for (int i = threadIdx.x; i < (RB + 1) * D; i += blockDim.x)
+    xs[i / D][i % D] = i < rows * D ? X[row0 * D + i] : 0.f;
   __syncthreads();
   const int R4 = r >> 2;
   for (int g = threadIdx.x; g < R4; g += blockDim.x) {
     float u[4][D];
+    if constexpr (D % 4 == 0) {
+      const float4* U4 = reinterpret_cast<const float4*>(U + (int64_t)4 * g * D);   // 4 rows of U
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+      for (int j = 0; j < D; ++j) {   // 4 * D floats = D float4
+        const float4 t = U4[j];
+        u[(4 * j) / D][(4 * j) % D] = t.x;
+        u[(4 * j) / D][(4 * j) % D + 1] = t.y;
+        u[(4 * j) / D][(4 * j) % D + 2] = t.z;
+        u[(4 * j) / D][(4 * j) % D + 3] = t.w;
+      }
+    } else {
 #pragma unroll
-      for (int c = 0; c < D; ++c) u[q][c] = U[(int64_t)(4 * g + q) * D + c];
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < D; ++c) u[q][c] = U[(int64_t)(4 * g + q) * D + c];
+    }
     const float4 bd = *reinterpret_cast<const float4*>(betaD + 4 * g);
     const float bq[4] = {bd.x, bd.y, bd.z, bd.w};
+    float xc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xc[c] = xs[0][c];
+#pragma unroll 2
     for (int i = 0; i < rows; ++i) {
+      float xn[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xn[c] = xs[i + 1][c];
       float o[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float sq = 0.f;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float df = xs[i][c] - u[q][c];
+          const float df = xc[c] - u[q][c];
           sq = fmaf(df, df, sq);
         }
         o[q] = ex2(fmaf(c2, sq, bq[q]));
       }
       st_global_cs(reinterpret_cast<float4*>(Xi + (row0 + i) * r) + g, make_float4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+      for (int c = 0; c < D; ++c) xc[c] = xn[c];
     }
   }
 }
@@ -227,9 +254,8 @@ cudaError_t launch_feature_map(const float* X, int64_t n, int d, const float* U,
   const float c2 = (float)(-2.0 * kLog2e / eps);
   if (n <= 0) return cudaSuccess;
   if (d <= 16) {
-    const int blocks = (int)((n + 31) / 32);
     switch (d) {
-#define CASE(DD) case DD: feature_map_direct_kernel<DD><<<blocks, 256, 0, s>>>(X, n, U, betaD, r, c2, Xi); break;
+#define CASE(DD) case DD: feature_map_direct_kernel<DD><<<(unsigned)((n + DirectRows<DD>::value - 1) / DirectRows<DD>::value), 256, 0, s>>>(X, n, U, betaD, r, c2, Xi); break;
       CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
       CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE

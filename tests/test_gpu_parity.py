@@ -183,7 +183,7 @@ def test_implicit_exponent_forms(L, cfg_key, n, m, T, R, eps):
     selected by the data through an explicit R >= max |p| (the map is valid for any such R,
     PAPER.md:385-391), against the oracle with the same R (ragged n, m: tail tiles).  The
     tuning-build alternatives (warp-private, hybrid, pipelined) are checked by
-    scripts/tuning_parity.py against the tuning library."""
+    tests/tools/tuning_parity.py against the tuning library."""
     cfg = synth.get_config(cfg_key)
     if R > 0.0:
         assert 1.4426950408889634 / eps * R * R > 60.0

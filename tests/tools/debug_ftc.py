@@ -1,5 +1,6 @@
 import os, sys
-sys.path.insert(0, "/root/repo")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle as O, paper_2006_07057_b200 as L
 for (M, r, d) in [(128, 128, 32), (128, 128, 64), (256, 128, 128), (777, 512, 128)]:

@@ -1,7 +1,7 @@
 """Probe: smallest eps the fp32 GPU path handles on the config-2 generator (n = m = 4000,
 r = 1000) vs the fp64 oracle."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle as O, synth
 import paper_2006_07057_b200 as L

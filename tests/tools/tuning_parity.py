@@ -2,11 +2,11 @@
 `python paper_2006_07057_b200/build.py --tuning`) against the fp64 oracle: the implicit
 kernel's expanded exponent forced (LSK_FACT=0) and every instantiated alternative
 configuration (pipelined teams, warp-private kernel, the round-1 hybrid with stream warps).
-The product liblsk.so contains none of these.  usage (GPU): python scripts/tuning_parity.py"""
+The product liblsk.so contains none of these.  usage (GPU): python tests/tools/tuning_parity.py"""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["LSK_LIB_PATH"] = os.path.join(ROOT, "scripts", "variants", "liblsk_tuning.so")
 sys.path.insert(0, ROOT)
 
