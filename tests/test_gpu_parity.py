@@ -115,6 +115,35 @@ def test_feature_map_matches_oracle(L, cfg_key, n):
     assert np.all(got >= 0)
 
 
+@pytest.mark.parametrize("d,r,n", [(4, 132, 33), (7, 100, 65), (8, 132, 1), (8, 2052, 63), (9, 100, 64),
+                                   (12, 1028, 65), (16, 132, 130), (16, 2052, 129)])
+def test_feature_map_direct_shapes(L, d, r, n):
+    """The FFMA direct-form map (d <= 16, DESIGN.md §6 K2): both row-block sizes (32 rows for
+    d < 8, 64 for d >= 8) with one row, one row short of a block, a full block, one row over;
+    the float4 (4 | d) and the scalar anchor loads; threads with no, one and three column groups."""
+    import torch
+    rng = np.random.default_rng(d * 1000 + r + n)
+    X = (rng.normal(size=(n, d)) / math.sqrt(d)).astype(np.float32)
+    R = float(np.max(np.linalg.norm(X.astype(np.float64), axis=1)))
+    eps = 0.5
+    p = L.lsk_feature_params_init(eps, d, r, R, 777)
+    U = torch.empty((r, d), dtype=torch.float32, device="cuda")
+    L.lsk_draw_anchors(p, U)
+    Xi = torch.full((n + 1, r), -1.0, dtype=torch.float32, device="cuda")   # guard row
+    L.lsk_feature_map(p, U, _dev(X), Xi[:n])
+    torch.cuda.synchronize()
+    assert bool((Xi[n] == -1.0).all())                     # nothing written past row n
+    prm = O.gaussian_params(eps, d, r, R)
+    Uo = O.draw_anchors(r, d, prm["sigma"], 777)
+    ref = O.feature_matrix(X, Uo, eps, prm["q"]).T
+    got = Xi[:n].cpu().double().numpy()
+    mask = ref > 1e-30
+    assert mask.mean() > 0.5
+    rel = np.abs(got[mask] - ref[mask]) / ref[mask]
+    assert rel.max() <= 3e-5, rel.max()
+    assert np.all(got[~mask] < 1e-29) and np.all(got >= 0)
+
+
 @pytest.mark.parametrize("d,r,n", [(40, 100, 1000), (100, 640, 129), (127, 256, 300),
                                    (128, 512, 4099), (17, 132, 257), (128, 1000, 513)])
 def test_feature_map_tensor_core_shapes(L, d, r, n):
