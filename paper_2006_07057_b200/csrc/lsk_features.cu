@@ -129,11 +129,17 @@ cudaError_t launch_anchor_prep(const float* U, int r, int d, double eps, double 
 
 // ---------------------------------------------------------------- a3: feature map --------
 // d <= 16, direct form: e2 = betaD_k + c2 * sum_c (x_ic - U_kc)^2, xi = 2^e2.
-// Block = 256 threads x RB rows (32 for d < 8, where the kernel is write-bound; 64 for d >= 8,
+// Block = 256 threads x RB rows (32 for d < 8, where the kernel is write-bound; 128 for d >= 8,
 // where the anchor loads per column group are amortised over more rows); thread t owns float4
 // column groups t, t+256, ...  The next row's coordinates are read from shared memory while
 // the current row is computed (one row ahead, in registers).
-template <int D> struct DirectRows { static constexpr int value = D >= 8 ? 64 : 32; };
+#ifndef LSK_DIRECT_RB
+#define LSK_DIRECT_RB 128
+#endif
+#ifndef LSK_DIRECT_UNROLL
+#define LSK_DIRECT_UNROLL 1
+#endif
+template <int D> struct DirectRows { static constexpr int value = D >= 8 ? LSK_DIRECT_RB : 32; };
 
 template <int D>
 __global__ void __launch_bounds__(256) feature_map_direct_kernel(
@@ -170,7 +176,8 @@ __global__ void __launch_bounds__(256) feature_map_direct_kernel(
     float xc[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) xc[c] = xs[0][c];
-#pragma unroll 2
+    constexpr int kUnroll = LSK_DIRECT_UNROLL;
+#pragma unroll kUnroll
     for (int i = 0; i < rows; ++i) {
       float xn[D];
 #pragma unroll

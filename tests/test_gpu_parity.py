@@ -115,11 +115,11 @@ def test_feature_map_matches_oracle(L, cfg_key, n):
     assert np.all(got >= 0)
 
 
-@pytest.mark.parametrize("d,r,n", [(4, 132, 33), (7, 100, 65), (8, 132, 1), (8, 2052, 63), (9, 100, 64),
-                                   (12, 1028, 65), (16, 132, 130), (16, 2052, 129)])
+@pytest.mark.parametrize("d,r,n", [(4, 132, 33), (7, 100, 65), (8, 132, 1), (8, 2052, 127), (9, 100, 128),
+                                   (12, 1028, 129), (16, 132, 300), (16, 2052, 257)])
 def test_feature_map_direct_shapes(L, d, r, n):
     """The FFMA direct-form map (d <= 16, DESIGN.md §6 K2): both row-block sizes (32 rows for
-    d < 8, 64 for d >= 8) with one row, one row short of a block, a full block, one row over;
+    d < 8, 128 for d >= 8) with one row, one row short of a block, a full block, one row over;
     the float4 (4 | d) and the scalar anchor loads; threads with no, one and three column groups."""
     import torch
     rng = np.random.default_rng(d * 1000 + r + n)
