@@ -118,10 +118,14 @@ __global__ void __launch_bounds__(256) grad_accum_kernel(const float* __restrict
 
 // fixed-order reduction of the CTA partials: acc[k][j] = sum_cta part[cta][k][j]
 // (block of 32 elements x 8 warps: warp w adds parts w, w+8, ... in order, then the 8 warp
-// sums in order — deterministic and 8x the loads in flight of a thread-per-element loop)
+// sums in order — deterministic and 8x the loads in flight of a thread-per-element loop).
+// blockIdx.y selects the factor: the partial arrays of xi and zeta are contiguous, and so are
+// their sums (one launch for both).
 __global__ void __launch_bounds__(256) grad_reduce_kernel(const double* __restrict__ part,
                                                           int nparts, int64_t len,
                                                           double* __restrict__ acc) {
+  part += (int64_t)blockIdx.y * nparts * len;
+  acc += (int64_t)blockIdx.y * len;
   __shared__ double red[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -279,8 +283,7 @@ cudaError_t launch_gradients(const float* X, int64_t n, const float* Y, int64_t 
   case DD:                                                                                       \
     ACCUM(DD, Xi, n, u, X, partx)                                                                \
     ACCUM(DD, Zeta, m, v, Y, party)                                                              \
-    grad_reduce_kernel<<<red_blocks, 256, 0, s>>>(partx, kAccCtas, len, accx);                   \
-    grad_reduce_kernel<<<red_blocks, 256, 0, s>>>(party, kAccCtas, len, accy);                   \
+    grad_reduce_kernel<<<dim3(red_blocks, 2), 256, 0, s>>>(partx, kAccCtas, len, accx);          \
     if (gX) ROWS_NV(DD, Xi, n, u, X, accy, gX)                                                   \
     if (gY) ROWS_NV(DD, Zeta, m, v, Y, accx, gY)                                                 \
     break;
@@ -293,7 +296,7 @@ cudaError_t launch_gradients(const float* X, int64_t n, const float* Y, int64_t 
     default:
       return cudaErrorInvalidValue;
   }
-  count_launch(4 + (gX ? 1 : 0) + (gY ? 1 : 0));
+  count_launch(3 + (gX ? 1 : 0) + (gY ? 1 : 0));
   if (gU) {
     grad_anchor_kernel<<<(r + 127) / 128, 128, 0, s>>>(accx, accy, U, r, d, q, gU);
     count_launch();
